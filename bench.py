@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""bench.py -- elements integrated per second on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...           (N > 1)
+
+Headline workload (N=1, BASELINE.json configs[1] -> SURVEY config C2):
+generalized convection-diffusion-reaction on 4,088,832 linear tetrahedra
+(88^3 Kuhn cells), per-element coefficients, fp64, natural QSS geo_linear
+descriptor.  One step = one ``fek_integrate`` launch over the whole batch.
+Scaling is weak: every rank integrates its own C2-sized range of a
+(rank-seeded) mesh, base_index = rank*n, no collective on the hot path.
+
+Printed JSON (rank 0, one line):
+  value      whole-job elements/s, inputs already in HBM (device events, max
+             over ranks; 1.7 GB of traffic per step >> 126 MB L2);
+  e2e        same metric through the public API ``integrate_batch(desc,
+             host_batch)`` with page-locked host buffers: H2D + kernel + D2H
+             inside the timed region;
+  roofline   of the integration kernel (algorithmic bytes / launch time vs the
+             measured HBM copy peak);
+  cpu_baseline  the reference algorithm (oracle port) on all host cores;
+  cases      C1/C3/C4 (fp64, C4 also fp32) kernel timings + rooflines;
+  parity     GPU vs CPU oracle on the full C2 batch and on case samples.
+
+``--impl reference`` times the reference's CPU algorithm (oracle port) on the
+same workload, on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "elements integrated/sec (fp64) at 1/2/4/8 B200; % of HBM/FP64 roofline"
+UNIT = "elements/s"
+L2_BYTES = 126 * 2 ** 20
+
+
+def parse(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[1])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--cases", default="C1,C3,C4,C4f32", help="extra per-config kernel timings (N=1 only)")
+    ap.add_argument("--no-cases", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-processes", type=int, default=None)
+    ap.add_argument("--variant", default="qss", choices=("qss", "sqs", "ssq"))
+    return ap.parse_args(argv)
+
+
+def _config_record(cfg, n_per_rank, world, desc, extra=None):
+    rec = {
+        "workload": f"{cfg.key}: {cfg.text}",
+        "mesh": f"{cfg.spec.nx}x{cfg.spec.ny}x{cfg.spec.nz} {cfg.spec.element_type.value}",
+        "elements_per_gpu": n_per_rank,
+        "elements_total": n_per_rank * world,
+        "descriptor": desc.short_name(),
+        "layout": "element-major",
+        "parallelism": f"element-range shards x{world} (no collective on the hot path)",
+        "l2": f"per-step traffic {n_per_rank * 416 / 1e9:.2f} GB > {L2_BYTES / 2**20:.0f} MiB L2 (no reuse)",
+    }
+    if extra:
+        rec.update(extra)
+    return rec
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
+def run_reference(args) -> int:
+    from oracle.cpu_baseline import PortPool, cpu_cores
+    from paper_1504_01023_b200 import KernelDescriptor, mesh, natural_path
+    from paper_1504_01023_b200.distributed import env_rank
+    from paper_1504_01023_b200.problems import Variant
+
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    cfg = mesh.bench_configs()[args.config]
+    et, pb = cfg.spec.element_type, cfg.problem
+    desc = KernelDescriptor(Variant(args.variant), natural_path(et), pb, et)
+    geo, cof = mesh.config_rows(cfg)
+    n = geo.shape[0]
+    cores = cpu_cores()
+    procs = args.cpu_processes or cores["logical"] or 1
+    sample = min(n, 1 << 19)
+    times = []
+    with PortPool(desc.variant.value, desc.geometry_path.value, pb.value, et.value, geo, cof, procs) as pool:
+        for _ in range(max(args.warmup, 0)):
+            pool.run(0, min(sample, 65536))
+        for k in range(args.steps):
+            lo = (k * sample) % max(1, n - sample + 1)
+            times.append(pool.run(lo, lo + sample))
+    sec = float(np.mean(times))
+    value = sample / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference mesh generator, seeded coefficients)",
+        "config": _config_record(cfg, n, 1, desc, {"sample_elements_per_step": sample}),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
+                         "sample": f"{sample} contiguous elements of {cfg.key} per step (oracle port of "
+                                   f"feklab integrate_batch, {procs} processes)", "host_cores": cores},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+class Launcher:
+    """Prepared fek_integrate call on device tensors (no Python work per launch but ctypes)."""
+
+    def __init__(self, desc, geo, cof, base_index=0, layout=None):
+        import torch
+
+        from paper_1504_01023_b200 import ELEMENT_MAJOR, _native
+        from paper_1504_01023_b200.kernels.batched import _desc_struct
+
+        self.lib = _native.load()
+        et = desc.element
+        ns = et.n_shape
+        n = geo.numel() // et.geometry_size
+        self.n = n
+        self.A = torch.empty((n, ns, ns), dtype=geo.dtype, device=geo.device)
+        self.b = torch.empty((n, ns), dtype=geo.dtype, device=geo.device)
+        self.err = torch.full((1,), -1, dtype=torch.int64, device=geo.device)
+        self.keep = (geo, cof)
+        code = _native.DTYPE["float64" if geo.dtype == torch.float64 else "float32"]
+        self.dd = _desc_struct(desc, layout or ELEMENT_MAJOR, n, base_index, code, geo.data_ptr(), cof.data_ptr(),
+                               self.A.data_ptr(), self.b.data_ptr(), self.err.data_ptr())
+        self.ref = ctypes.byref(self.dd)
+        self.stream = torch.cuda.current_stream().cuda_stream
+
+    def __call__(self):
+        rc = self.lib.fek_integrate(self.ref, self.stream)
+        if rc:
+            from paper_1504_01023_b200 import _native
+
+            _native.check(rc, "fek_integrate")
+
+    def error_key(self) -> int:
+        return int(self.err.item()) & 0xFFFFFFFFFFFFFFFF
+
+
+def time_launches(launchers, steps, warmup, sampler=None):
+    """Per-launch device times (ms) over `steps` launches cycling through `launchers`."""
+    import torch
+
+    for k in range(warmup):
+        launchers[k % len(launchers)]()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    t_all = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    ctx = sampler if sampler is not None else _Null()
+    with ctx:
+        t_all[0].record()
+        for k in range(steps):
+            evs[k][0].record()
+            launchers[k % len(launchers)]()
+            evs[k][1].record()
+        t_all[1].record()
+        torch.cuda.synchronize()
+    per = [a.elapsed_time(b) for a, b in evs]
+    return per, t_all[0].elapsed_time(t_all[1])
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def sample_parity(desc, geo_rows, cof_rows, A_dev, b_dev, count=8192, seed=0):
+    """Max relative Frobenius error of GPU outputs vs the oracle on `count` sampled elements."""
+    from oracle import numpy_oracle as O
+
+    n = geo_rows.shape[0]
+    idx = np.unique(np.random.default_rng(seed).integers(0, n, size=min(count, n)))
+    import torch
+
+    it = torch.from_numpy(idx).to(A_dev.device)
+    A = A_dev.index_select(0, it).double().cpu().numpy()
+    b = b_dev.index_select(0, it).double().cpu().numpy()
+    Ao, bo = O.integrate(desc.variant.value, desc.geometry_path.value, desc.problem.value, desc.element.value,
+                         geo_rows[idx], cof_rows[idx])
+    return float(max(O.rel_frobenius(A, Ao).max(), O.rel_frobenius(b, bo).max())), int(idx.size)
+
+
+def measure_case(key, steps, warmup, variant="qss"):
+    import torch
+
+    from paper_1504_01023_b200 import KernelDescriptor, mesh, natural_path
+    from paper_1504_01023_b200.measure import case_roofline
+    from paper_1504_01023_b200.problems import Variant
+
+    fp32 = key.endswith("f32")
+    cfg = mesh.bench_configs()[key.replace("f32", "")]
+    et, pb = cfg.spec.element_type, cfg.problem
+    desc = KernelDescriptor(Variant(variant), natural_path(et), pb, et)
+    geo_rows, cof_rows = mesh.config_rows(cfg)
+    n = geo_rows.shape[0]
+    dt = torch.float32 if fp32 else torch.float64
+    geo = torch.from_numpy(geo_rows.reshape(-1)).to("cuda", dtype=dt)
+    cof = torch.from_numpy(cof_rows.reshape(-1)).to("cuda", dtype=dt)
+    rb = 4 if fp32 else 8
+    per_set = n * (et.geometry_size + pb.coefficient_size(et) + et.n_shape * (et.n_shape + 1)) * rb
+    sets = 1 if per_set > 3 * L2_BYTES else 3  # rotate buffer sets when one set is near L2 size
+    launchers = [Launcher(desc, geo, cof)]
+    for _ in range(sets - 1):
+        launchers.append(Launcher(desc, geo.clone(), cof.clone()))
+    per, _ = time_launches(launchers, steps, warmup)
+    for L in launchers:
+        if L.error_key() != 0xFFFFFFFFFFFFFFFF:
+            raise RuntimeError(f"{key}: unexpected geometry error key {L.error_key():#x}")
+    ms = float(np.mean(per))
+    err, cnt = sample_parity(desc, geo_rows, cof_rows, launchers[0].A, launchers[0].b)
+    tol = 1e-3 if fp32 else 1e-12
+    rec = {
+        "workload": cfg.text + (" (fp32)" if fp32 else " (fp64)"),
+        "elements": n, "descriptor": desc.short_name(), "dtype": "f32" if fp32 else "f64",
+        "value": n / (ms / 1e3), "unit": UNIT, "ms_per_launch": ms, "ms_min": float(np.min(per)),
+        "buffer_sets": sets,
+        "roofline": case_roofline(et, pb, n, ms / 1e3, rb),
+        "parity": {"max_rel_frobenius": err, "elements_checked": cnt, "tolerance": tol, "pass": err <= tol,
+                   "against": "numpy oracle (bitwise-pinned restatement of the reference)"},
+    }
+    del launchers, geo, cof
+    torch.cuda.empty_cache()
+    return rec
+
+
+def load_profile_traffic(kernel_tag: str):
+    """Per-launch dram bytes from the committed ncu summary, if present."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            data = json.load(fh)
+        return data.get(kernel_tag, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_ours(args) -> int:
+    import torch
+    import torch.distributed as dist
+
+    from oracle import numpy_oracle as O
+    from paper_1504_01023_b200 import (DeviceBatch, ElementBatch, KernelDescriptor, integrate_batch, launch_config,
+                                       mesh, natural_path)
+    from paper_1504_01023_b200.distributed import env_rank
+    from paper_1504_01023_b200.measure import ClockSampler, case_roofline, clocks_rejected
+    from paper_1504_01023_b200.problems import Variant
+
+    rank, world, local = env_rank()
+    if not torch.cuda.is_available():
+        print(json.dumps({"metric": METRIC, "error": "no CUDA device"}))
+        return 1
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    cfg = mesh.bench_configs()[args.config]
+    et, pb = cfg.spec.element_type, cfg.problem
+    desc = KernelDescriptor(Variant(args.variant), natural_path(et), pb, et)
+    geo_rows = mesh.geometry_rows(cfg.spec)
+    cof_rows = mesh.coefficient_rows(cfg.spec.n_elements, pb, et, cfg.coeff_seed + rank)
+    n = geo_rows.shape[0]
+    host_batch = ElementBatch.from_arrays(et, pb, geo_rows, cof_rows)      # page-locked flat arrays
+    dev_batch = DeviceBatch.from_host(host_batch)
+    launcher = Launcher(desc, dev_batch.geometry_data, dev_batch.coefficient_data, base_index=rank * n)
+
+    # ---- device-resident timing (the `value`) ----
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    per, total_ms = time_launches([launcher], args.steps, args.warmup, sampler)
+    key = launcher.error_key()
+    if key != 0xFFFFFFFFFFFFFFFF:
+        raise RuntimeError(f"geometry error key {key:#x} in the benchmark mesh")
+    step_ms = total_ms / args.steps
+    launch_ms = float(np.mean(per))
+    t = torch.tensor([step_ms, launch_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms, launch_ms = t.tolist()
+    value = world * n / (step_ms / 1e3)
+    clocks = sampler.summary()
+    reject = clocks_rejected(clocks)
+
+    # ---- end-to-end through the public API on host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e_steps = max(1, min(args.steps, 10))
+        integrate_batch(desc, host_batch)  # warm (pinned result blocks, streams, workspace)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(e2e_steps):
+            res = integrate_batch(desc, host_batch, base_index=rank * n)
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / e2e_steps
+        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        h2d = host_batch.geometry_data.nbytes + host_batch.coefficient_data.nbytes
+        d2h = res.stiffness.nbytes + res.load.nbytes
+        host_equal = bool(np.array_equal(res.stiffness, launcher.A.cpu().numpy()))
+        e2e = {"value": world * n / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ms, "steps": e2e_steps,
+               "api": "paper_1504_01023_b200.integrate_batch(desc, ElementBatch) -> BatchResult (numpy)",
+               "bitwise_equal_to_device_path": host_equal}
+
+    out = None
+    if rank == 0:
+        cfgd = launch_config(desc, host_batch.layout, n)
+        roof = case_roofline(et, pb, n, launch_ms / 1e3)
+        kernel_tag = f"{desc.short_name()}_f64"
+        roof_line = {"bound": roof["bound"], "achieved": roof["achieved"], "peak": roof["peak"],
+                     "unit": roof["unit"], "frac": roof["frac"], "traffic": load_profile_traffic(kernel_tag),
+                     "algorithmic_bytes_per_launch": roof["bytes_per_launch"],
+                     "peak_source": roof["peak_source"], "kernel": f"fek::integrate_kernel<{kernel_tag}>",
+                     "launch_ms": launch_ms, "launch_ms_min": float(np.min(per)), **cfgd}
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic: reference unit-cube Kuhn mesh, numpy default_rng(seed+rank) U(-1,1) coefficients",
+               "config": _config_record(cfg, n, world, desc), "clocks": clocks, "e2e": e2e,
+               "gpu_launches": args.steps, "roofline": roof_line}
+        if reject:
+            out["clocks_warning"] = reject
+
+    # ---- CPU baseline + full-size parity (rank 0, N=1) ----
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle.cpu_baseline import PortPool, cpu_cores
+
+        cores = cpu_cores()
+        procs = args.cpu_processes or cores["logical"] or 1
+        with PortPool(desc.variant.value, desc.geometry_path.value, pb.value, et.value, geo_rows, cof_rows,
+                      procs) as pool:
+            pool.run(0, min(n, 65536))
+            sec = pool.run(0, n)
+            A_cpu, b_cpu = pool.A, pool.b
+            A_gpu = launcher.A.cpu().numpy()
+            b_gpu = launcher.b.cpu().numpy()
+            errA = float(O.rel_frobenius(A_gpu, A_cpu).max())
+            errb = float(O.rel_frobenius(b_gpu, b_cpu).max())
+        out["cpu_baseline"] = {"value": n / sec, "unit": UNIT, "cores": procs, "kind": "port",
+                               "sample": f"full {cfg.key} batch ({n} elements) once, oracle port of feklab "
+                                         f"integrate_batch on {procs} processes", "seconds": sec,
+                               "host_cores": cores}
+        out["parity"] = {"workload": cfg.key, "elements_checked": n, "max_rel_frobenius_A": errA,
+                         "max_rel_frobenius_b": errb, "tolerance": 1e-12, "pass": max(errA, errb) <= 1e-12,
+                         "against": "numpy oracle, bitwise-pinned to the reference (tests/golden)"}
+
+    # ---- other configurations (N=1) ----
+    if rank == 0 and world == 1 and not args.no_cases:
+        del dev_batch
+        cases = {}
+        for key in [c for c in args.cases.split(",") if c]:
+            try:
+                cases[key] = measure_case(key, args.steps, args.warmup)
+            except Exception as exc:  # keep the headline line even if a case fails
+                cases[key] = {"error": f"{type(exc).__name__}: {exc}"}
+        out["cases"] = cases
+
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None) -> int:
+    args = parse(argv)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

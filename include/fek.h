@@ -1,0 +1,142 @@
+/*
+ * fek.h -- C-ABI of libfek.so: B200 (sm_100a) element integration for
+ * first-order tetrahedra and prisms (arXiv 1504.01023).
+ *
+ * This is the drop-in boundary for the reference's hot path.  Each entry
+ * point names the reference interface it replaces (paths relative to
+ * /root/reference/pkg/src/feklab):
+ *
+ *   fek_integrate       <- kernels/batched.py:518-533  the _BATCHED_KERNELS
+ *                          registry slot + _run_range block loop, i.e. the body
+ *                          of integrate_batch (batched.py:536-606) after the
+ *                          layout decode; device buffers, stream-ordered.
+ *   fek_integrate_host  <- kernels/batched.py:536-606  integrate_batch as a
+ *                          whole, on HOST arrays (ElementBatch.geometry_data /
+ *                          coefficient_data in, BatchResult.stiffness / load
+ *                          out): chunked H2D -> kernel -> D2H pipeline.
+ *   fek_decode_error    <- errors.py:8-27 + batched.py:166-177,593-599  the
+ *                          first-error rule (element, quadrature point, kind).
+ *   fek_error_detail    <- batched.py:172-177  the |det J| / tol numbers that
+ *                          go into the DegenerateElement/InvertedElement text.
+ *   fek_checksum        <- (new) per-shard verification sums reduced with
+ *                          NCCL across GPUs.
+ *
+ * Conventions
+ *  - Plain C types only.  All device pointers are caller-owned (PyTorch
+ *    allocations in the Python host layer); the library never allocates
+ *    device memory and keeps no mutable global state besides a per-kernel
+ *    attribute cache, so calls are safe from several host threads on
+ *    distinct streams.
+ *  - Input layout (batch flat arrays) follows layout.py:1-23:
+ *      element-major:        datum d of element e at e*DS + d
+ *      lane-interleaved (W): (e/W)*W*DS + d*W + e%W   (tail padded to W)
+ *    Outputs are element-major: stiffness (n, ns, ns) row-major, load (n, ns)
+ *    (batched.py:566-567).
+ *  - Base pointers must be 16-byte aligned.
+ *  - Results are bitwise independent of layout, lane width, launch chunking
+ *    and base_index sharding: every element runs the same instruction
+ *    sequence (batched.py:10-13 promises the same for workers/layout).
+ */
+#ifndef FEK_H
+#define FEK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FEK_ABI_VERSION 1
+
+/* enums mirror the Python ones (refelem.py:29, problems.py:26-49) */
+enum fek_element { FEK_TETRAHEDRON = 0, FEK_PRISM = 1 };
+enum fek_problem { FEK_POISSON = 0, FEK_CONV_DIFF = 1 };
+enum fek_variant { FEK_QSS = 0, FEK_SQS = 1, FEK_SSQ = 2 };
+enum fek_geometry_path { FEK_GEO_LINEAR = 0, FEK_GEO_GENERIC = 1 };
+enum fek_dtype { FEK_F64 = 0, FEK_F32 = 1 };
+enum fek_layout_kind { FEK_ELEMENT_MAJOR = 0, FEK_LANE_INTERLEAVED = 1 };
+
+/* status codes */
+enum fek_status {
+  FEK_OK = 0,
+  FEK_ERR_ARGUMENT = 1,      /* bad enum / size / combination            */
+  FEK_ERR_ALIGNMENT = 2,     /* a base pointer is not 16-byte aligned      */
+  FEK_ERR_CUDA = 3,          /* CUDA runtime error (see fek_last_cuda_error) */
+  FEK_ERR_WORKSPACE = 4,     /* host-pipeline workspace too small          */
+  FEK_ERR_GEOMETRY = 5       /* fek_integrate_host: a degenerate/inverted element */
+};
+
+/* error word: all-ones = no error; smaller key = earlier error */
+#define FEK_NO_ERROR 0xFFFFFFFFFFFFFFFFull
+#define FEK_KIND_DEGENERATE 1
+#define FEK_KIND_INVERTED 2
+#define FEK_KIND_PIPELINE_TIMEOUT 3
+
+typedef struct fek_batch_desc {
+  int32_t element;        /* enum fek_element                                   */
+  int32_t problem;        /* enum fek_problem                                   */
+  int32_t variant;        /* enum fek_variant                                   */
+  int32_t geometry_path;  /* enum fek_geometry_path (LINEAR requires TETRAHEDRON) */
+  int32_t dtype;          /* enum fek_dtype: real type of all four arrays        */
+  int32_t layout;         /* enum fek_layout_kind of geometry/coefficients       */
+  int32_t lane_width;     /* W in {1,4,8,16,32,64}; 1 for element-major         */
+  int32_t reserved;
+  int64_t n_elements;     /* elements covered by this call                       */
+  int64_t base_index;     /* absolute index of element 0 (errors, sharding)      */
+  const void *geometry;   /* flat geometry_data  (3*nv reals per element)        */
+  const void *coefficients; /* flat coefficient_data (nq or 20 reals)            */
+  void *stiffness;        /* (n, ns, ns) reals                                   */
+  void *load;             /* (n, ns) reals                                       */
+  unsigned long long *error_key; /* device word (fek_integrate), init FEK_NO_ERROR */
+} fek_batch_desc;
+
+int fek_abi_version(void);
+const char *fek_status_string(int status);
+/* message of the last CUDA error seen by this thread (empty if none) */
+const char *fek_last_cuda_error(void);
+
+/* Stream-ordered integration of d->n_elements elements; all pointers device.
+ * Asynchronous: returns after the launch.  Geometry failures are recorded
+ * with atomicMin into *d->error_key (the reference's first-error rule). */
+int fek_integrate(const fek_batch_desc *d, void *cuda_stream);
+
+/* Launch geometry fek_integrate would use (for reporting / launch counting). */
+int fek_launch_config(const fek_batch_desc *d, int *grid, int *block, int *smem_bytes,
+                      int *tile_elements);
+
+/* Whole-batch integration on HOST buffers (d->geometry/coefficients/stiffness/
+ * load are host pointers, ideally page-locked; d->error_key is ignored).
+ * Elements stream through `n_streams` slots of `chunk_elements` each, carved
+ * from the device workspace: chunk i is copied H2D, integrated and copied D2H
+ * on streams[i % n_streams], so the copy engines and the SMs overlap.
+ * Blocks until done.  On a geometry failure returns FEK_ERR_GEOMETRY and
+ * stores the error key in *error_key_out (FEK_NO_ERROR otherwise). */
+size_t fek_host_workspace_bytes(const fek_batch_desc *d, int n_streams, int64_t chunk_elements);
+int fek_integrate_host(const fek_batch_desc *d, void *device_workspace, size_t workspace_bytes,
+                       int n_streams, void *const *cuda_streams, int64_t chunk_elements,
+                       unsigned long long *error_key_out);
+
+/* Split an error key.  point = -1 on the element-constant (geo_linear) path. */
+int fek_decode_error(unsigned long long key, int64_t *element, int32_t *point, int32_t *kind);
+
+/* det J and the degeneracy tolerance of local element `element` of d at
+ * quadrature point `point` (-1: affine Jacobian), written to out_det_tol[0..1]
+ * (device memory).  Used only to format error messages. */
+int fek_error_detail(const fek_batch_desc *d, int64_t element, int32_t point,
+                     double *out_det_tol, void *cuda_stream);
+
+/* Verification sums over d's outputs, written to device memory:
+ * out_f64[0..3] = sum A, sum b, sum |A|, sum |b| (fixed-order, deterministic);
+ * out_u64[0..1] = wrapping sums of the IEEE bit patterns of A and b entries,
+ * each weighted by (absolute element index + 1): exactly additive across
+ * shards, so an NCCL SUM of per-GPU values equals the single-GPU value
+ * bit for bit.  `partials` is device scratch of fek_checksum_scratch_bytes(). */
+size_t fek_checksum_scratch_bytes(void);
+int fek_checksum(const fek_batch_desc *d, void *partials, double *out_f64,
+                 unsigned long long *out_u64, void *cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FEK_H */

@@ -1,0 +1,7 @@
+// kernel instantiations: f32 tet poisson (all variants / geometry paths)
+#define FEK_CASE_TU 1
+#include "../fek_dispatch.cuh"
+
+namespace fek {
+void register_f32_tet_poisson(KernelEntry *table) { fill_case<float, TET, POISSON>(table, FEK_F32); }
+}  // namespace fek

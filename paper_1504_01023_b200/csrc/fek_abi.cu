@@ -1,0 +1,407 @@
+// fek_abi.cu -- C-ABI of libfek.so (include/fek.h): descriptor validation,
+// kernel dispatch, the host-buffer pipeline, error decoding and checksums.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/fek.h"
+#include "fek_dispatch.cuh"
+
+namespace {
+
+using fek::KernelEntry;
+using fek::kIndexCount;
+using fek::kernel_index;
+using fek::LaunchParams;
+
+thread_local char g_cuda_error[256] = "";
+
+int cuda_fail(cudaError_t e, const char *what) {
+  std::snprintf(g_cuda_error, sizeof(g_cuda_error), "%s: %s", what, cudaGetErrorString(e));
+  return FEK_ERR_CUDA;
+}
+
+#define FEK_CUDA(call)                              \
+  do {                                              \
+    cudaError_t _e = (call);                        \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+// kernels are instantiated per case in cases/*.cu (parallel compilation)
+const KernelEntry *kernel_table() {
+  static KernelEntry table[kIndexCount];
+  static std::once_flag once;
+  std::call_once(once, [] {
+    fek::register_f64_tet_poisson(table);
+    fek::register_f64_tet_convdiff(table);
+    fek::register_f64_prism_poisson(table);
+    fek::register_f64_prism_convdiff(table);
+    fek::register_f32_tet_poisson(table);
+    fek::register_f32_tet_convdiff(table);
+    fek::register_f32_prism_poisson(table);
+    fek::register_f32_prism_convdiff(table);
+  });
+  return table;
+}
+
+// per (device, kernel) launch geometry, computed once
+struct LaunchGeometry {
+  int ready = 0;
+  int resident = 0;  // CTAs per SM
+  int sms = 0;
+};
+constexpr int kMaxDevices = 16;
+LaunchGeometry g_geometry[kMaxDevices][kIndexCount];
+std::mutex g_geometry_mutex;
+
+int launch_geometry(int idx, const KernelEntry &ke, LaunchGeometry *out) {
+  int dev = 0;
+  FEK_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return FEK_ERR_ARGUMENT;
+  std::lock_guard<std::mutex> lock(g_geometry_mutex);
+  LaunchGeometry &lg = g_geometry[dev][idx];
+  if (!lg.ready) {
+    FEK_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void *>(ke.fn),
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ke.smem)));
+    FEK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lg.resident, ke.fn, ke.threads, ke.smem));
+    FEK_CUDA(cudaDeviceGetAttribute(&lg.sms, cudaDevAttrMultiProcessorCount, dev));
+    if (lg.resident < 1) lg.resident = 1;
+    lg.ready = 1;
+  }
+  *out = lg;
+  return FEK_OK;
+}
+
+int n_shape(int et) { return et == FEK_TETRAHEDRON ? 4 : 6; }
+int n_quad(int et) { return et == FEK_TETRAHEDRON ? 4 : 6; }
+int geometry_size(int et) { return 3 * n_shape(et); }
+int coefficient_size(int et, int pb) { return pb == FEK_POISSON ? n_quad(et) : 20; }
+int real_bytes(int dtype) { return dtype == FEK_F64 ? 8 : 4; }
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int validate(const fek_batch_desc *d, bool need_pointers) {
+  if (!d) return FEK_ERR_ARGUMENT;
+  if (d->element < 0 || d->element > 1 || d->problem < 0 || d->problem > 1) return FEK_ERR_ARGUMENT;
+  if (d->variant < 0 || d->variant > 2 || d->geometry_path < 0 || d->geometry_path > 1) return FEK_ERR_ARGUMENT;
+  if (d->dtype < 0 || d->dtype > 1) return FEK_ERR_ARGUMENT;
+  if (d->geometry_path == FEK_GEO_LINEAR && d->element != FEK_TETRAHEDRON) return FEK_ERR_ARGUMENT;
+  if (d->layout == FEK_ELEMENT_MAJOR) {
+    if (d->lane_width != 1) return FEK_ERR_ARGUMENT;
+  } else if (d->layout == FEK_LANE_INTERLEAVED) {
+    const int w = d->lane_width;
+    if (!(w == 1 || w == 4 || w == 8 || w == 16 || w == 32 || w == 64)) return FEK_ERR_ARGUMENT;
+  } else {
+    return FEK_ERR_ARGUMENT;
+  }
+  if (d->n_elements < 0 || d->base_index < 0) return FEK_ERR_ARGUMENT;
+  if (need_pointers && d->n_elements > 0) {
+    if (!d->geometry || !d->coefficients || !d->stiffness || !d->load) return FEK_ERR_ARGUMENT;
+    if (!aligned16(d->geometry) || !aligned16(d->coefficients) || !aligned16(d->stiffness) || !aligned16(d->load))
+      return FEK_ERR_ALIGNMENT;
+  }
+  return FEK_OK;
+}
+
+int launch(const fek_batch_desc *d, cudaStream_t stream, int *grid_out, int *block_out, int *smem_out,
+           int *tile_out, bool do_launch) {
+  const int idx = kernel_index(d->dtype, d->element, d->problem, d->variant, d->geometry_path);
+  const KernelEntry &ke = kernel_table()[idx];
+  if (!ke.fn) return FEK_ERR_ARGUMENT;
+  LaunchGeometry lg;
+  if (int rc = launch_geometry(idx, ke, &lg)) return rc;
+  const long long tiles = (d->n_elements + ke.tile - 1) / ke.tile;
+  const long long cap = static_cast<long long>(lg.sms) * lg.resident;
+  const int grid = static_cast<int>(tiles < cap ? tiles : cap);
+  if (grid_out) *grid_out = grid;
+  if (block_out) *block_out = ke.threads;
+  if (smem_out) *smem_out = static_cast<int>(ke.smem);
+  if (tile_out) *tile_out = ke.tile;
+  if (!do_launch || grid == 0) return FEK_OK;
+  LaunchParams p;
+  p.geometry = d->geometry;
+  p.coefficients = d->coefficients;
+  p.stiffness = d->stiffness;
+  p.load = d->load;
+  p.error_key = d->error_key;
+  p.n = d->n_elements;
+  p.base = d->base_index;
+  p.lane_width = d->layout == FEK_ELEMENT_MAJOR ? 1 : d->lane_width;
+  ke.fn<<<grid, ke.threads, ke.smem, stream>>>(p);
+  FEK_CUDA(cudaGetLastError());
+  return FEK_OK;
+}
+
+// --------------------------------------------------------------------------
+// checksum kernels (deterministic fixed-order reduction)
+// --------------------------------------------------------------------------
+
+constexpr int kSumBlocks = 592;  // 148 SMs x 4
+constexpr int kSumThreads = 256;
+
+template <typename R>
+__device__ __forceinline__ unsigned long long real_bits(R v) {
+  if constexpr (sizeof(R) == 8) {
+    return static_cast<unsigned long long>(__double_as_longlong(v));
+  } else {
+    return static_cast<unsigned long long>(__float_as_uint(v));
+  }
+}
+
+template <typename R>
+__global__ void __launch_bounds__(kSumThreads) checksum_partials(const R *A, const R *b, long long n, int na,
+                                                                 int ns, long long base, double *part_f,
+                                                                 unsigned long long *part_u) {
+  __shared__ double sf[4][kSumThreads];
+  __shared__ unsigned long long su[2][kSumThreads];
+  const long long per = (n + gridDim.x - 1) / gridDim.x;
+  const long long lo = per * blockIdx.x;
+  const long long hi = lo + per < n ? lo + per : n;
+  double f[4] = {0, 0, 0, 0};
+  unsigned long long u[2] = {0, 0};
+  for (long long i = lo * na + threadIdx.x; i < hi * na; i += blockDim.x) {
+    const R v = A[i];
+    f[0] += static_cast<double>(v);
+    f[2] += fabs(static_cast<double>(v));
+    u[0] += real_bits(v) * (2ull * static_cast<unsigned long long>(base * na + i) + 1ull);
+  }
+  for (long long i = lo * ns + threadIdx.x; i < hi * ns; i += blockDim.x) {
+    const R v = b[i];
+    f[1] += static_cast<double>(v);
+    f[3] += fabs(static_cast<double>(v));
+    u[1] += real_bits(v) * (2ull * static_cast<unsigned long long>(base * ns + i) + 1ull);
+  }
+  for (int k = 0; k < 4; ++k) sf[k][threadIdx.x] = f[k];
+  su[0][threadIdx.x] = u[0];
+  su[1][threadIdx.x] = u[1];
+  __syncthreads();
+  for (int stride = kSumThreads / 2; stride > 0; stride >>= 1) {
+    if (threadIdx.x < stride) {
+      for (int k = 0; k < 4; ++k) sf[k][threadIdx.x] += sf[k][threadIdx.x + stride];
+      su[0][threadIdx.x] += su[0][threadIdx.x + stride];
+      su[1][threadIdx.x] += su[1][threadIdx.x + stride];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 4; ++k) part_f[4 * blockIdx.x + k] = sf[k][0];
+    part_u[2 * blockIdx.x] = su[0][0];
+    part_u[2 * blockIdx.x + 1] = su[1][0];
+  }
+}
+
+__global__ void checksum_final(const double *part_f, const unsigned long long *part_u, int blocks, double *out_f,
+                               unsigned long long *out_u) {
+  if (threadIdx.x != 0) return;
+  double f[4] = {0, 0, 0, 0};
+  unsigned long long u[2] = {0, 0};
+  for (int i = 0; i < blocks; ++i) {
+    for (int k = 0; k < 4; ++k) f[k] += part_f[4 * i + k];
+    u[0] += part_u[2 * i];
+    u[1] += part_u[2 * i + 1];
+  }
+  for (int k = 0; k < 4; ++k) out_f[k] = f[k];
+  out_u[0] = u[0];
+  out_u[1] = u[1];
+}
+
+}  // namespace
+
+extern "C" {
+
+int fek_abi_version(void) { return FEK_ABI_VERSION; }
+
+const char *fek_status_string(int status) {
+  switch (status) {
+    case FEK_OK: return "ok";
+    case FEK_ERR_ARGUMENT: return "invalid argument";
+    case FEK_ERR_ALIGNMENT: return "base pointer not 16-byte aligned";
+    case FEK_ERR_CUDA: return "CUDA runtime error";
+    case FEK_ERR_WORKSPACE: return "workspace too small";
+    case FEK_ERR_GEOMETRY: return "degenerate or inverted element";
+    default: return "unknown status";
+  }
+}
+
+const char *fek_last_cuda_error(void) { return g_cuda_error; }
+
+int fek_integrate(const fek_batch_desc *d, void *cuda_stream) {
+  if (int rc = validate(d, true)) return rc;
+  if (d->n_elements > 0 && !d->error_key) return FEK_ERR_ARGUMENT;
+  return launch(d, static_cast<cudaStream_t>(cuda_stream), nullptr, nullptr, nullptr, nullptr, true);
+}
+
+int fek_launch_config(const fek_batch_desc *d, int *grid, int *block, int *smem_bytes, int *tile_elements) {
+  if (int rc = validate(d, false)) return rc;
+  return launch(d, nullptr, grid, block, smem_bytes, tile_elements, false);
+}
+
+int fek_decode_error(unsigned long long key, int64_t *element, int32_t *point, int32_t *kind) {
+  if (key == FEK_NO_ERROR) return FEK_ERR_ARGUMENT;
+  const unsigned long long blk = key >> 24;
+  const int q = static_cast<int>((key >> 20) & 15ull);
+  const unsigned long long within = (key >> 7) & 8191ull;
+  if (element) *element = static_cast<int64_t>((blk << fek::ERROR_BLOCK_SHIFT) | within);
+  if (point) *point = q == 15 ? -1 : q;
+  if (kind) *kind = static_cast<int32_t>(key & 3ull);
+  return FEK_OK;
+}
+
+int fek_error_detail(const fek_batch_desc *d, int64_t element, int32_t point, double *out_det_tol,
+                     void *cuda_stream) {
+  if (int rc = validate(d, false)) return rc;
+  if (!d->geometry || !out_det_tol || element < 0 || element >= d->n_elements) return FEK_ERR_ARGUMENT;
+  const int w = d->layout == FEK_ELEMENT_MAJOR ? 1 : d->lane_width;
+  const int nq = n_quad(d->element);
+  if (point >= nq) return FEK_ERR_ARGUMENT;
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  if (d->dtype == FEK_F64) {
+    if (d->element == FEK_TETRAHEDRON)
+      fek::error_detail_kernel<double, fek::TET><<<1, 1, 0, s>>>(d->geometry, element, w, point, out_det_tol);
+    else
+      fek::error_detail_kernel<double, fek::PRISM><<<1, 1, 0, s>>>(d->geometry, element, w, point, out_det_tol);
+  } else {
+    if (d->element == FEK_TETRAHEDRON)
+      fek::error_detail_kernel<float, fek::TET><<<1, 1, 0, s>>>(d->geometry, element, w, point, out_det_tol);
+    else
+      fek::error_detail_kernel<float, fek::PRISM><<<1, 1, 0, s>>>(d->geometry, element, w, point, out_det_tol);
+  }
+  FEK_CUDA(cudaGetLastError());
+  return FEK_OK;
+}
+
+size_t fek_checksum_scratch_bytes(void) { return static_cast<size_t>(kSumBlocks) * (4 * 8 + 2 * 8); }
+
+int fek_checksum(const fek_batch_desc *d, void *partials, double *out_f64, unsigned long long *out_u64,
+                 void *cuda_stream) {
+  if (int rc = validate(d, false)) return rc;
+  if (!partials || !out_f64 || !out_u64) return FEK_ERR_ARGUMENT;
+  if (d->n_elements > 0 && (!d->stiffness || !d->load)) return FEK_ERR_ARGUMENT;
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  double *pf = static_cast<double *>(partials);
+  unsigned long long *pu = reinterpret_cast<unsigned long long *>(pf + 4 * kSumBlocks);
+  const int ns = n_shape(d->element);
+  if (d->dtype == FEK_F64) {
+    checksum_partials<double><<<kSumBlocks, kSumThreads, 0, s>>>(
+        static_cast<const double *>(d->stiffness), static_cast<const double *>(d->load), d->n_elements, ns * ns,
+        ns, d->base_index, pf, pu);
+  } else {
+    checksum_partials<float><<<kSumBlocks, kSumThreads, 0, s>>>(
+        static_cast<const float *>(d->stiffness), static_cast<const float *>(d->load), d->n_elements, ns * ns,
+        ns, d->base_index, pf, pu);
+  }
+  checksum_final<<<1, 32, 0, s>>>(pf, pu, kSumBlocks, out_f64, out_u64);
+  FEK_CUDA(cudaGetLastError());
+  return FEK_OK;
+}
+
+// --------------------------------------------------------------------------
+// host-buffer pipeline
+// --------------------------------------------------------------------------
+
+namespace {
+struct SlotPlan {
+  size_t geo, coef, A, b, slot;
+};
+
+size_t round256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
+
+SlotPlan slot_plan(const fek_batch_desc *d, long long chunk) {
+  const size_t rb = real_bytes(d->dtype);
+  const int ns = n_shape(d->element);
+  SlotPlan p;
+  p.geo = round256(chunk * geometry_size(d->element) * rb);
+  p.coef = round256(chunk * coefficient_size(d->element, d->problem) * rb);
+  p.A = round256(chunk * ns * ns * rb);
+  p.b = round256(chunk * ns * rb);
+  p.slot = p.geo + p.coef + p.A + p.b;
+  return p;
+}
+
+long long flat_len(long long n, int ds, int w) { return n == 0 ? 0 : ((n + w - 1) / w) * w * ds; }
+}  // namespace
+
+size_t fek_host_workspace_bytes(const fek_batch_desc *d, int n_streams, int64_t chunk_elements) {
+  if (!d || n_streams < 1 || chunk_elements < 1) return 0;
+  return 256 + static_cast<size_t>(n_streams) * slot_plan(d, chunk_elements).slot;
+}
+
+int fek_integrate_host(const fek_batch_desc *d, void *device_workspace, size_t workspace_bytes, int n_streams,
+                       void *const *cuda_streams, int64_t chunk_elements, unsigned long long *error_key_out) {
+  if (int rc = validate(d, false)) return rc;
+  if (n_streams < 1 || !cuda_streams || chunk_elements < 1 || !error_key_out) return FEK_ERR_ARGUMENT;
+  const int w = d->layout == FEK_ELEMENT_MAJOR ? 1 : d->lane_width;
+  // chunk boundaries on whole lane blocks and even element counts (fp32 rows)
+  const long long align = 128;  // TILE: multiple of every lane width
+  long long chunk = ((chunk_elements + align - 1) / align) * align;
+  if (fek_host_workspace_bytes(d, n_streams, chunk) > workspace_bytes || !device_workspace)
+    return FEK_ERR_WORKSPACE;
+  if (!aligned16(device_workspace)) return FEK_ERR_ALIGNMENT;
+  *error_key_out = FEK_NO_ERROR;
+  const long long n = d->n_elements;
+  if (n == 0) return FEK_OK;
+  if (!d->geometry || !d->coefficients || !d->stiffness || !d->load) return FEK_ERR_ARGUMENT;
+
+  char *ws = static_cast<char *>(device_workspace);
+  unsigned long long *dkey = reinterpret_cast<unsigned long long *>(ws);
+  const SlotPlan sp = slot_plan(d, chunk);
+  const size_t rb = real_bytes(d->dtype);
+  const int dsg = geometry_size(d->element), dsc = coefficient_size(d->element, d->problem);
+  const int ns = n_shape(d->element);
+  cudaStream_t s0 = static_cast<cudaStream_t>(cuda_streams[0]);
+
+  // error word initialised on stream 0; the other streams wait for it
+  FEK_CUDA(cudaMemsetAsync(dkey, 0xFF, sizeof(unsigned long long), s0));
+  cudaEvent_t ready;
+  FEK_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  FEK_CUDA(cudaEventRecord(ready, s0));
+  for (int i = 1; i < n_streams; ++i)
+    FEK_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(cuda_streams[i]), ready, 0));
+
+  const char *hg = static_cast<const char *>(d->geometry);
+  const char *hc = static_cast<const char *>(d->coefficients);
+  char *hA = static_cast<char *>(d->stiffness);
+  char *hb = static_cast<char *>(d->load);
+  int rc = FEK_OK;
+  long long ci = 0;
+  for (long long lo = 0; lo < n && rc == FEK_OK; lo += chunk, ++ci) {
+    const long long cnt = (n - lo) < chunk ? (n - lo) : chunk;
+    const int slot = static_cast<int>(ci % n_streams);
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_streams[slot]);
+    char *base = ws + 256 + slot * sp.slot;
+    char *dg = base, *dc = base + sp.geo, *dA = dc + sp.coef, *db = dA + sp.A;
+    // lo is a multiple of 128 (hence of W): the chunk's flat range starts at lo*DS
+    const size_t gbytes = flat_len(cnt, dsg, w) * rb, cbytes = flat_len(cnt, dsc, w) * rb;
+    cudaError_t e = cudaMemcpyAsync(dg, hg + lo * dsg * rb, gbytes, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dc, hc + lo * dsc * rb, cbytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) {
+      rc = cuda_fail(e, "cudaMemcpyAsync H2D");
+      break;
+    }
+    fek_batch_desc cd = *d;
+    cd.n_elements = cnt;
+    cd.base_index = d->base_index + lo;
+    cd.geometry = dg;
+    cd.coefficients = dc;
+    cd.stiffness = dA;
+    cd.load = db;
+    cd.error_key = dkey;
+    rc = launch(&cd, st, nullptr, nullptr, nullptr, nullptr, true);
+    if (rc) break;
+    e = cudaMemcpyAsync(hA + lo * ns * ns * rb, dA, cnt * ns * ns * rb, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hb + lo * ns * rb, db, cnt * ns * rb, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync D2H");
+  }
+  for (int i = 0; i < n_streams; ++i) {
+    cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(cuda_streams[i]));
+    if (e != cudaSuccess && rc == FEK_OK) rc = cuda_fail(e, "cudaStreamSynchronize");
+  }
+  cudaEventDestroy(ready);
+  if (rc) return rc;
+  FEK_CUDA(cudaMemcpy(error_key_out, dkey, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  return *error_key_out == FEK_NO_ERROR ? FEK_OK : FEK_ERR_GEOMETRY;
+}
+
+}  // extern "C"

@@ -1,0 +1,60 @@
+// fek_dispatch.cuh -- kernel table shared by fek_abi.cu and the per-case
+// translation units in cases/ (one TU per dtype x element x problem, so the
+// 28 kernel instantiations compile in parallel).
+#pragma once
+
+#include "../../include/fek.h"
+#include "fek_kernel.cuh"
+
+namespace fek {
+
+using KernelFn = void (*)(const LaunchParams);
+
+struct KernelEntry {
+  KernelFn fn = nullptr;
+  unsigned smem = 0;
+  int threads = 0;
+  int tile = 0;
+};
+
+// index: dtype(2) x element(2) x problem(2) x variant(3) x path(2)
+constexpr int kIndexCount = 2 * 2 * 2 * 3 * 2;
+inline int kernel_index(int dtype, int et, int pb, int var, int geo) {
+  return (((dtype * 2 + et) * 2 + pb) * 3 + var) * 2 + geo;
+}
+
+void register_f64_tet_poisson(KernelEntry *table);
+void register_f64_tet_convdiff(KernelEntry *table);
+void register_f64_prism_poisson(KernelEntry *table);
+void register_f64_prism_convdiff(KernelEntry *table);
+void register_f32_tet_poisson(KernelEntry *table);
+void register_f32_tet_convdiff(KernelEntry *table);
+void register_f32_prism_poisson(KernelEntry *table);
+void register_f32_prism_convdiff(KernelEntry *table);
+
+#ifdef FEK_CASE_TU
+template <class K>
+KernelEntry entry() {
+  KernelEntry e;
+  e.fn = integrate_kernel<K>;
+  e.smem = K::SMEM_BYTES;
+  e.threads = K::THREADS;
+  e.tile = K::TILE;
+  return e;
+}
+
+template <typename R, int ET, int PB>
+void fill_case(KernelEntry *table, int dtype) {
+  table[kernel_index(dtype, ET, PB, QSS, GEO_GENERIC)] = entry<Traits<R, ET, PB, QSS, GEO_GENERIC>>();
+  table[kernel_index(dtype, ET, PB, SQS, GEO_GENERIC)] = entry<Traits<R, ET, PB, SQS, GEO_GENERIC>>();
+  table[kernel_index(dtype, ET, PB, SSQ, GEO_GENERIC)] = entry<Traits<R, ET, PB, SSQ, GEO_GENERIC>>();
+  if constexpr (ET == TET) {
+    // the reference's three geo_linear loop nests are one hoisted arithmetic
+    // (bitwise equal in the reference itself): one kernel serves all three
+    const KernelEntry lin = entry<Traits<R, ET, PB, QSS, GEO_LINEAR>>();
+    for (int v = 0; v < 3; ++v) table[kernel_index(dtype, ET, PB, v, GEO_LINEAR)] = lin;
+  }
+}
+#endif
+
+}  // namespace fek

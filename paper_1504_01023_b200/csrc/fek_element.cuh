@@ -1,0 +1,485 @@
+// fek_element.cuh -- per-element integration math, one thread per element.
+//
+// Reference semantics (paths under /root/reference/pkg/src/feklab):
+//   geometry  : bbox scale batched.py:136-148; adjugate/det :151-163;
+//               degeneracy/inversion check :166-177 (|det| <= 1e-14*diag^3
+//               first, then det < 0); inverse = adj * (1/det) :180-182;
+//               affine Jacobian columns v_{k+1}-v_0 :185-190; per-point
+//               Jacobian X^T * ld_q :193-207; global derivatives :210-220.
+//   Poisson   : A_rs = sum_q vol_q g_r.g_s, b_r = sum_q vol_q phi_r(q) d0[q]
+//               (_PoissonBatch :238-251, symmetric mirror :373-380).
+//   ConvDiff  : A_rs = sum_q vol_q sum_ij c_ij phi^i_r phi^j_s,
+//               b_r = sum_q vol_q sum_i d_i phi^i_r (_ConvDiffBatch :254-275).
+//   geo_linear: q-invariant parts hoisted out of the q loop (_linear_terms
+//               :352-358, _ConvDiffLinear :298-335); the remaining q-sums of
+//               tabulated basis values are the precomputed quadrature moments
+//               WSUM/MV/MVV/WV of refconst.h.
+//   variants  : QSS / SQS / SSQ loop nests of the generic path (:434-515);
+//               SQS recomputes the point data per row, SSQ per entry, exactly
+//               as the reference's loop skeletons do.
+//
+// Arithmetic is written with explicit fma() and the library is compiled with
+// --fmad=false, so every element runs one fixed instruction sequence: results
+// are bitwise independent of tile position, layout, chunking and GPU count.
+// They differ from the reference's numpy evaluation order by rounding only
+// (relative Frobenius ~1e-15, tolerance 1e-12 per SPEC).
+#pragma once
+
+#include <cstdint>
+
+#include "fek_device.cuh"
+#include "refconst.h"
+
+namespace fek {
+
+enum : int { TET = 0, PRISM = 1 };
+enum : int { POISSON = 0, CONV_DIFF = 1 };
+enum : int { QSS = 0, SQS = 1, SSQ = 2 };
+enum : int { GEO_LINEAR = 0, GEO_GENERIC = 1 };
+
+constexpr unsigned long long NO_ERROR = 0xFFFFFFFFFFFFFFFFull;
+constexpr int KIND_DEGENERATE = 1;
+constexpr int KIND_INVERTED = 2;
+constexpr int KIND_PIPELINE_TIMEOUT = 3;
+constexpr int ERROR_BLOCK_SHIFT = 13;  // batched.py:50 BLOCK_ELEMENTS = 8192
+
+// Error key ordering = the reference's first-error rule (batched.py:528-533,
+// :166-177): earliest 8192-element block, then smallest quadrature point
+// inside the block (15 = affine / no point), then lowest element.
+__host__ __device__ __forceinline__ unsigned long long make_error_key(long long element, int point,
+                                                                      int kind) {
+  const unsigned long long blk = static_cast<unsigned long long>(element) >> ERROR_BLOCK_SHIFT;
+  const unsigned long long within = static_cast<unsigned long long>(element) & 8191ull;
+  const unsigned long long q = point < 0 ? 15ull : static_cast<unsigned long long>(point);
+  return (blk << 24) | (q << 20) | (within << 7) | static_cast<unsigned long long>(kind);
+}
+
+// ---------------------------------------------------------------------------
+// element geometry helpers
+// ---------------------------------------------------------------------------
+
+template <int ET>
+struct Shape;
+template <>
+struct Shape<TET> {
+  static constexpr int NV = 4, NS = 4, NQ = 4;
+  __host__ __device__ static constexpr double w(int q) { return refconst::TET_W[q]; }
+  __host__ __device__ static constexpr double val(int q, int s) { return refconst::TET_VAL[q][s]; }
+  __host__ __device__ static constexpr double ld(int q, int s, int k) { return refconst::TET_LD[q][s][k]; }
+};
+template <>
+struct Shape<PRISM> {
+  static constexpr int NV = 6, NS = 6, NQ = 6;
+  __host__ __device__ static constexpr double w(int q) { return refconst::PRISM_W[q]; }
+  __host__ __device__ static constexpr double val(int q, int s) { return refconst::PRISM_VAL[q][s]; }
+  __host__ __device__ static constexpr double ld(int q, int s, int k) { return refconst::PRISM_LD[q][s][k]; }
+};
+
+template <typename R>
+__device__ __forceinline__ R rmax(R a, R b) {
+  return a > b ? a : b;
+}
+template <typename R>
+__device__ __forceinline__ R rmin(R a, R b) {
+  return a < b ? a : b;
+}
+
+// 1e-14 * (bounding-box diagonal)^3   (geometry.py:22-24, batched.py:136-148)
+template <typename R, int NV>
+__device__ __forceinline__ R degeneracy_tolerance(const R *X) {
+  R acc = R(0);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    R hi = X[i], lo = X[i];
+#pragma unroll
+    for (int v = 1; v < NV; ++v) {
+      hi = fmax(hi, X[3 * v + i]);
+      lo = fmin(lo, X[3 * v + i]);
+    }
+    const R span = hi - lo;
+    acc = fma(span, span, acc);
+  }
+  const R scale = sqrt(acc);
+  return R(1e-14) * (scale * scale * scale);
+}
+
+// cofactor adjugate + determinant of J[i][k] (row i = physical x_i,
+// column k = reference xi_k), batched.py:151-163
+template <typename R>
+struct Jac {
+  R inv[3][3];  // inv[k][i] = d xi_k / d x_i
+  R det;
+};
+
+template <typename R>
+__device__ __forceinline__ Jac<R> invert3(const R (&J)[3][3]) {
+  const R a = J[0][0], b = J[0][1], c = J[0][2];
+  const R d = J[1][0], e = J[1][1], f = J[1][2];
+  const R g = J[2][0], h = J[2][1], i = J[2][2];
+  const R k00 = fma(e, i, -(f * h));
+  const R k01 = fma(f, g, -(d * i));
+  const R k02 = fma(d, h, -(e * g));
+  Jac<R> out;
+  out.det = fma(a, k00, fma(b, k01, c * k02));
+  const R r = R(1) / out.det;
+  out.inv[0][0] = k00 * r;
+  out.inv[0][1] = fma(c, h, -(b * i)) * r;
+  out.inv[0][2] = fma(b, f, -(c * e)) * r;
+  out.inv[1][0] = k01 * r;
+  out.inv[1][1] = fma(a, i, -(c * g)) * r;
+  out.inv[1][2] = fma(c, d, -(a * f)) * r;
+  out.inv[2][0] = k02 * r;
+  out.inv[2][1] = fma(b, g, -(a * h)) * r;
+  out.inv[2][2] = fma(a, e, -(b * d)) * r;
+  return out;
+}
+
+// degenerate first, then inverted; NaN determinants pass (as in numpy)
+template <typename R>
+__device__ __forceinline__ int classify(R det, R tol) {
+  if (fabs(det) <= tol) return KIND_DEGENERATE;
+  if (det < R(0)) return KIND_INVERTED;
+  return 0;
+}
+
+// sum_k c_k * x_k over compile-time coefficients, skipping zeros and using
+// +-1 as add/sub (the reference's _axpy_fixed, batched.py:119-133)
+template <typename R>
+struct Lin {
+  R acc;
+  bool any = false;
+  template <int DUMMY = 0>
+  __device__ __forceinline__ void add(double c, R x) {
+    if (c == 0.0) return;
+    if (!any) {
+      acc = (c == 1.0) ? x : (c == -1.0 ? -x : R(c) * x);
+      any = true;
+    } else if (c == 1.0) {
+      acc = acc + x;
+    } else if (c == -1.0) {
+      acc = acc - x;
+    } else {
+      acc = fma(R(c), x, acc);
+    }
+  }
+  __device__ __forceinline__ R get() const { return any ? acc : R(0); }
+};
+
+#define FEK_CI(name, ic) constexpr int name = decltype(ic)::value
+
+// Per-point Jacobian at compile-time point Q: J[i][k] = sum_v ld[Q][v][k] X[v][i]
+template <int ET, int Q, typename R>
+__device__ __forceinline__ void point_jacobian(const R *X, R (&J)[3][3]) {
+  using S = Shape<ET>;
+  static_for<3>([&](auto ic) {
+    FEK_CI(i, ic);
+    static_for<3>([&](auto kc) {
+      FEK_CI(k, kc);
+      Lin<R> acc;
+      static_for<S::NV>([&](auto vc) {
+        FEK_CI(v, vc);
+        acc.add(S::ld(Q, v, k), X[3 * v + i]);
+      });
+      J[i][k] = acc.get();
+    });
+  });
+}
+
+// Global derivatives of shape function SF at point Q: g[i] = sum_k ld[Q][SF][k] inv[k][i]
+template <int ET, int Q, int SF, typename R>
+__device__ __forceinline__ void global_grad(const Jac<R> &jac, R (&g)[3]) {
+  using S = Shape<ET>;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    Lin<R> t;
+    static_for<3>([&](auto kc) {
+      FEK_CI(k, kc);
+      t.add(S::ld(Q, SF, k), jac.inv[k][i]);
+    });
+    g[i] = t.get();
+  }
+}
+
+template <int ET, int Q, typename R>
+__device__ __forceinline__ void all_grads(const Jac<R> &jac, R (&g)[Shape<ET>::NS][3]) {
+  static_for<Shape<ET>::NS>([&](auto sc) {
+    FEK_CI(s, sc);
+    global_grad<ET, Q, s>(jac, g[s]);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// geo_linear: tetrahedra, Jacobian once per element (all three variants:
+// the reference's _qss/_sqs/_ssq_linear are the same hoisted arithmetic)
+// ---------------------------------------------------------------------------
+
+template <typename R, int PB>
+__device__ __forceinline__ void integrate_tet_linear(const R (&X)[12], const R *coef, R (&A)[16],
+                                                     R (&B)[4], int &kind) {
+  using namespace refconst;
+  R J[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) J[i][k] = X[3 * (k + 1) + i] - X[i];
+  const Jac<R> jac = invert3(J);
+  kind = classify(jac.det, degeneracy_tolerance<R, 4>(X));
+  const R det = jac.det;
+  // g[s][i]: shape 0 has local gradient (-1,-1,-1), shape k+1 the unit e_k
+  R g[4][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    g[1][i] = jac.inv[0][i];
+    g[2][i] = jac.inv[1][i];
+    g[3][i] = jac.inv[2][i];
+    g[0][i] = -((jac.inv[0][i] + jac.inv[1][i]) + jac.inv[2][i]);
+  }
+  constexpr R wsum = R(TET_WSUM);
+  if constexpr (PB == POISSON) {
+    const R vt = det * wsum;
+    static_for<4>([&](auto rc) {
+      FEK_CI(r, rc);
+#pragma unroll
+      for (int s = r; s < 4; ++s) {
+        const R gg = fma(g[r][0], g[s][0], fma(g[r][1], g[s][1], g[r][2] * g[s][2]));
+        A[4 * r + s] = vt * gg;
+        A[4 * s + r] = A[4 * r + s];
+      }
+      constexpr R wv0 = R(TET_WV[0][r]);
+      R acc = wv0 * coef[0];
+      static_for<3>([&](auto qc) {
+        FEK_CI(q, qc);
+        constexpr R wv = R(TET_WV[q + 1][r]);
+        acc = fma(wv, coef[q + 1], acc);
+      });
+      B[r] = det * acc;
+    });
+  } else {
+    // coef row: c00 c01 c02 c03 c10 ... c33 d0 d1 d2 d3 (problems.py:136-140)
+    const R *c = coef;
+    const R *d = coef + 16;
+    R Cg[4][3], row0[4], col0[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        Cg[s][i] = fma(c[4 * (i + 1) + 1], g[s][0], fma(c[4 * (i + 1) + 2], g[s][1], c[4 * (i + 1) + 3] * g[s][2]));
+      row0[s] = fma(c[1], g[s][0], fma(c[2], g[s][1], c[3] * g[s][2]));
+      col0[s] = fma(c[4], g[s][0], fma(c[8], g[s][1], c[12] * g[s][2]));
+    }
+    const R c00 = c[0];
+    static_for<4>([&](auto rc) {
+      FEK_CI(r, rc);
+      static_for<4>([&](auto sc) {
+        FEK_CI(s, sc);
+        const R dd = fma(g[r][0], Cg[s][0], fma(g[r][1], Cg[s][1], g[r][2] * Cg[s][2]));
+        constexpr R mvv = R(TET_MVV[r][s]), mvs = R(TET_MV[s]), mvr = R(TET_MV[r]);
+        R t = mvv * c00;
+        t = fma(mvs, col0[r], t);
+        t = fma(mvr, row0[s], t);
+        t = fma(wsum, dd, t);
+        A[4 * r + s] = det * t;
+      });
+      const R dg = fma(d[1], g[r][0], fma(d[2], g[r][1], d[3] * g[r][2]));
+      constexpr R mvr = R(TET_MV[r]);
+      B[r] = det * fma(wsum, dg, mvr * d[0]);
+    });
+  }
+}
+
+// ---------------------------------------------------------------------------
+// geo_generic: Jacobian per quadrature point (prisms; tets on request)
+// ---------------------------------------------------------------------------
+
+// Point data at compile-time point Q from vertex coordinates X.
+template <int ET, int Q, typename R>
+struct PointData {
+  Jac<R> jac;
+  R vol;
+  int kind;
+  __device__ __forceinline__ PointData(const R *X, R tol) {
+    R J[3][3];
+    point_jacobian<ET, Q>(X, J);
+    jac = invert3(J);
+    kind = classify(jac.det, tol);
+    constexpr R w = R(Shape<ET>::w(Q));
+    vol = jac.det * w;
+  }
+};
+
+// ConvDiff t_s = vol * (C phi_s), phi_s = (val_s, g_s)
+template <typename R>
+__device__ __forceinline__ void cphi(const R *c, R val_s, const R (&g)[3], R vol, R (&t)[4]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const R x = fma(c[4 * i + 1], g[0], fma(c[4 * i + 2], g[1], fma(c[4 * i + 3], g[2], c[4 * i] * val_s)));
+    t[i] = vol * x;
+  }
+}
+
+template <typename R>
+__device__ __forceinline__ R dot4(R val_r, const R (&g)[3], const R (&t)[4]) {
+  return fma(val_r, t[0], fma(g[0], t[1], fma(g[1], t[2], g[2] * t[3])));
+}
+
+template <typename R>
+__device__ __forceinline__ R load_term(const R *d, R val_r, const R (&g)[3]) {
+  return fma(d[0], val_r, fma(d[1], g[0], fma(d[2], g[1], d[3] * g[2])));
+}
+
+// Geometry source for the generic path: each call returns the element's
+// vertex coordinates, either from registers or re-read from the staged
+// shared-memory tile (keeps ~36 registers free on the FP64-bound prism path
+// and, for SQS/SSQ, makes the per-row / per-entry recomputation real work as
+// in the reference's loop skeletons).
+template <typename R, int DS>
+struct RegGeometry {
+  const R (&X)[DS];
+  __device__ __forceinline__ void fetch(R (&out)[DS]) const {
+#pragma unroll
+    for (int i = 0; i < DS; ++i) out[i] = X[i];
+  }
+};
+
+template <typename R, int DS>
+struct SmemGeometry {
+  uint32_t tile;
+  int lane;
+  int width;
+  __device__ __forceinline__ void fetch(R (&out)[DS]) const { RowIO<R, DS>::load(tile, lane, width, out); }
+};
+
+template <typename R, int ET, int PB, int VAR, class Geo>
+__device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef, R tol,
+                                                  R (&A)[Shape<ET>::NS * Shape<ET>::NS],
+                                                  R (&B)[Shape<ET>::NS], int &kind, int &kind_point) {
+  using S = Shape<ET>;
+  constexpr int NS = S::NS, NQ = S::NQ, DSG = 3 * S::NV;
+  constexpr bool SYM = (PB == POISSON);
+  kind = 0;
+  kind_point = -1;
+  auto note = [&](int k, int q) {
+    if (k && !kind) {
+      kind = k;
+      kind_point = q;
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < NS * NS; ++i) A[i] = R(0);
+#pragma unroll
+  for (int i = 0; i < NS; ++i) B[i] = R(0);
+
+  if constexpr (VAR == QSS) {
+    static_for<NQ>([&](auto qc) {
+      FEK_CI(Q, qc);
+      R X[DSG];
+      geo.fetch(X);
+      const PointData<ET, Q, R> pd(X, tol);
+      note(pd.kind, Q);
+      R g[NS][3];
+      all_grads<ET, Q>(pd.jac, g);
+      if constexpr (SYM) {
+        static_for<NS>([&](auto rc) {
+          FEK_CI(r, rc);
+#pragma unroll
+          for (int s = r; s < NS; ++s) {
+            const R gg = fma(g[r][0], g[s][0], fma(g[r][1], g[s][1], g[r][2] * g[s][2]));
+            A[NS * r + s] = fma(pd.vol, gg, A[NS * r + s]);
+          }
+          constexpr R vr = R(S::val(Q, r));
+          B[r] = fma(pd.vol * vr, coef[Q], B[r]);
+        });
+      } else {
+        static_for<NS>([&](auto sc) {
+          FEK_CI(s, sc);
+          R t[4];
+          cphi(coef, R(S::val(Q, s)), g[s], pd.vol, t);
+          static_for<NS>([&](auto rc) {
+            FEK_CI(r, rc);
+            A[NS * r + s] += dot4(R(S::val(Q, r)), g[r], t);
+          });
+        });
+        static_for<NS>([&](auto rc) {
+          FEK_CI(r, rc);
+          B[r] = fma(pd.vol, load_term(coef + 16, R(S::val(Q, r)), g[r]), B[r]);
+        });
+      }
+    });
+  } else if constexpr (VAR == SQS) {
+    // row-at-a-time: point data recomputed for every (row, point)
+    static_for<NS>([&](auto rc) {
+      FEK_CI(r, rc);
+      static_for<NQ>([&](auto qc) {
+        FEK_CI(Q, qc);
+        R X[DSG];
+        geo.fetch(X);
+        const PointData<ET, Q, R> pd(X, tol);
+        note(pd.kind, Q);
+        R g[NS][3];
+        all_grads<ET, Q>(pd.jac, g);
+        if constexpr (SYM) {
+#pragma unroll
+          for (int s = r; s < NS; ++s) {
+            const R gg = fma(g[r][0], g[s][0], fma(g[r][1], g[s][1], g[r][2] * g[s][2]));
+            A[NS * r + s] = fma(pd.vol, gg, A[NS * r + s]);
+          }
+          constexpr R vr = R(S::val(Q, r));
+          B[r] = fma(pd.vol * vr, coef[Q], B[r]);
+        } else {
+          // row r: A_rs += vol * phi_r^T C phi_s = (vol C^T phi_r) . phi_s
+          constexpr R vr = R(S::val(Q, r));
+          R u[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            u[j] = pd.vol * fma(coef[4 + j], g[r][0], fma(coef[8 + j], g[r][1], fma(coef[12 + j], g[r][2], coef[j] * vr)));
+          static_for<NS>([&](auto sc) {
+            FEK_CI(s, sc);
+            A[NS * r + s] += dot4(R(S::val(Q, s)), g[s], u);
+          });
+          B[r] = fma(pd.vol, load_term(coef + 16, vr, g[r]), B[r]);
+        }
+      });
+    });
+  } else {
+    // entry-at-a-time: point data recomputed for every (row, column, point),
+    // only the two shape functions involved are differentiated
+    static_for<NS>([&](auto rc) {
+      FEK_CI(r, rc);
+      static_for<NS>([&](auto sc) {
+        FEK_CI(s, sc);
+        if constexpr (!SYM || s >= r) {
+          static_for<NQ>([&](auto qc) {
+            FEK_CI(Q, qc);
+            R X[DSG];
+            geo.fetch(X);
+            const PointData<ET, Q, R> pd(X, tol);
+            note(pd.kind, Q);
+            R gr[3], gs[3];
+            global_grad<ET, Q, r>(pd.jac, gr);
+            global_grad<ET, Q, s>(pd.jac, gs);
+            constexpr R vr = R(S::val(Q, r));
+            constexpr R vs = R(S::val(Q, s));
+            if constexpr (SYM) {
+              const R gg = fma(gr[0], gs[0], fma(gr[1], gs[1], gr[2] * gs[2]));
+              A[NS * r + s] = fma(pd.vol, gg, A[NS * r + s]);
+              if constexpr (r == s) B[r] = fma(pd.vol * vr, coef[Q], B[r]);
+            } else {
+              R t[4];
+              cphi(coef, vs, gs, pd.vol, t);
+              A[NS * r + s] += dot4(vr, gr, t);
+              if constexpr (r == s) B[r] = fma(pd.vol, load_term(coef + 16, vr, gr), B[r]);
+            }
+          });
+        }
+      });
+    });
+  }
+  if constexpr (SYM) {
+#pragma unroll
+    for (int r = 0; r < NS; ++r)
+#pragma unroll
+      for (int s = 0; s < r; ++s) A[NS * r + s] = A[NS * s + r];
+  }
+}
+
+}  // namespace fek

@@ -1,0 +1,377 @@
+"""Batch integration drop-in: ``integrate_batch`` on B200 through libfek.so.
+
+Mirror of ``pkg/src/feklab/kernels/batched.py:53-106,536-606``.  Same call,
+same result type, same errors:
+
+    integrate_batch(desc, batch, out_layout=ELEMENT_MAJOR, workers=1) -> BatchResult
+
+* ``batch`` may be a host ``ElementBatch`` (ours, or the reference's own —
+  fields are duck-typed) or a ``DeviceBatch`` whose flat arrays are CUDA
+  tensors.  Host batches stream through ``fek_integrate_host`` (chunked
+  H2D -> kernel -> D2H on three CUDA streams) and come back as numpy arrays,
+  so a reference caller sees no difference; device batches stay on the GPU
+  (``fek_integrate`` on the current torch stream) and return torch tensors.
+* ``workers`` is accepted for signature compatibility; the GPU decides the
+  parallel decomposition, and results are bitwise independent of it (as the
+  reference promises for its thread count, ``batched.py:10-13``).
+* A degenerate/inverted element raises ``DegenerateElement`` /
+  ``InvertedElement`` with the reference's element/point indices and message
+  text; there is no partial result (``batched.py:544-547``).
+* There is no CPU fallback: without the CUDA library or a GPU this raises
+  ``NativeLibraryError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .. import _native, hostmem
+from ..errors import DegenerateElement, InvertedElement, NativeLibraryError, ShapeMismatch
+from ..layout import ELEMENT_MAJOR, BatchLayout, LayoutKind, coerce_layout, flat_length, pack_rows
+from ..problems import (ElementMatrix, KernelDescriptor, ProblemClass, coerce_descriptor, coerce_element,
+                        coerce_problem)
+from ..refelem import ElementType
+
+HOST_STREAMS = 3
+
+
+@dataclass
+class TrafficCounters:
+    """Reals moved per batch (``batched.py:53-80``): inputs read once, outputs written once."""
+
+    geometry_reads: int = 0
+    coefficient_reads: int = 0
+    stiffness_writes: int = 0
+    load_writes: int = 0
+
+    @property
+    def total(self) -> int:
+        return self.geometry_reads + self.coefficient_reads + self.stiffness_writes + self.load_writes
+
+    def per_element(self, n_elements: int) -> float:
+        return self.total / n_elements
+
+    def breakdown_per_element(self, n_elements: int) -> tuple[float, float, float, float]:
+        return (self.geometry_reads / n_elements, self.coefficient_reads / n_elements,
+                self.stiffness_writes / n_elements, self.load_writes / n_elements)
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+@dataclass
+class BatchResult:
+    """Stiffness matrices (n, ns, ns) and load vectors (n, ns) of a batch.
+
+    numpy arrays for host batches, CUDA tensors for device batches.
+    """
+
+    descriptor: KernelDescriptor
+    n_elements: int
+    stiffness: object
+    load: object
+    traffic: TrafficCounters
+    out_layout: BatchLayout = field(default=ELEMENT_MAJOR)
+
+    def element_matrix(self, e: int) -> ElementMatrix:
+        if not 0 <= e < self.n_elements:
+            raise IndexError(f"element index {e} out of range")
+        A, b = self.stiffness[e], self.load[e]
+        if _is_torch(A):
+            A, b = A.detach().cpu().numpy(), b.detach().cpu().numpy()
+        return ElementMatrix(np.array(A, dtype=np.float64), np.array(b, dtype=np.float64))
+
+    def output_rows(self):
+        """(n, ns*ns + ns) rows: stiffness entries then load (``batched.py:99-102``)."""
+        n = self.n_elements
+        if _is_torch(self.stiffness):
+            import torch
+
+            return torch.cat([self.stiffness.reshape(n, -1), self.load], dim=1)
+        return np.concatenate([np.asarray(self.stiffness).reshape(n, -1), np.asarray(self.load)], axis=1)
+
+    def flat_output(self, pad_value: float = np.nan):
+        """Rows flattened in ``out_layout`` (``batched.py:104-106``); stays on the device for device results."""
+        rows = self.output_rows()
+        layout = coerce_layout(self.out_layout)
+        if not _is_torch(rows):
+            return pack_rows(rows, layout, pad_value)
+        import torch
+
+        n, ds = rows.shape
+        if layout.kind is LayoutKind.ELEMENT_MAJOR:
+            return rows.reshape(-1).clone()
+        w = layout.lane_width
+        out = torch.full((flat_length(n, ds, layout),), pad_value, dtype=rows.dtype, device=rows.device)
+        blocks = -(-n // w)
+        padded = torch.full((blocks * w, ds), pad_value, dtype=rows.dtype, device=rows.device)
+        padded[:n] = rows
+        out.copy_(padded.reshape(blocks, w, ds).transpose(1, 2).reshape(-1))
+        return out
+
+    def to_host(self) -> "BatchResult":
+        if not _is_torch(self.stiffness):
+            return self
+        return BatchResult(self.descriptor, self.n_elements, self.stiffness.cpu().numpy(),
+                           self.load.cpu().numpy(), self.traffic, self.out_layout)
+
+
+@dataclass(frozen=True)
+class DeviceBatch:
+    """A batch whose flat geometry/coefficient arrays are CUDA tensors (fp64 or fp32).
+
+    Same storage schemes as ``ElementBatch`` (``layout.py:1-23``).
+    """
+
+    element_type: ElementType
+    problem: ProblemClass
+    n_elements: int
+    layout: BatchLayout
+    geometry_data: object   # torch.Tensor, flat
+    coefficient_data: object
+
+    def __post_init__(self):
+        import torch
+
+        for name, t, ds in (("geometry_data", self.geometry_data, self.element_type.geometry_size),
+                            ("coefficient_data", self.coefficient_data,
+                             self.problem.coefficient_size(self.element_type))):
+            if not isinstance(t, torch.Tensor) or not t.is_cuda:
+                raise TypeError(f"{name} must be a CUDA tensor")
+            want = flat_length(self.n_elements, ds, self.layout)
+            if tuple(t.shape) != (want,) or not t.is_contiguous():
+                raise ValueError(f"{name} must be contiguous and flat with {want} entries, got {tuple(t.shape)}")
+            if t.dtype not in (torch.float64, torch.float32):
+                raise TypeError(f"{name} must be float64 or float32")
+        if self.geometry_data.dtype != self.coefficient_data.dtype:
+            raise TypeError("geometry and coefficient dtypes differ")
+
+    @property
+    def dtype(self):
+        return self.geometry_data.dtype
+
+    @classmethod
+    def from_host(cls, batch, device=None, dtype=None, non_blocking: bool = False) -> "DeviceBatch":
+        """Upload a host ``ElementBatch`` (optionally converting to float32)."""
+        import torch
+
+        device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        dtype = dtype or torch.float64
+
+        def up(a):
+            t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+            return t.to(device=device, dtype=dtype, non_blocking=non_blocking)
+
+        return cls(coerce_element(batch.element_type), coerce_problem(batch.problem), int(batch.n_elements),
+                   coerce_layout(batch.layout), up(batch.geometry_data), up(batch.coefficient_data))
+
+
+# ---------------------------------------------------------------------------
+# descriptor plumbing
+# ---------------------------------------------------------------------------
+
+def _desc_struct(desc: KernelDescriptor, layout: BatchLayout, n: int, base: int, dtype_code: int,
+                 geometry: int, coefficients: int, stiffness: int, load: int, error_key: int) -> _native.BatchDesc:
+    d = _native.BatchDesc()
+    d.element = _native.ELEMENT[desc.element.value]
+    d.problem = _native.PROBLEM[desc.problem.value]
+    d.variant = _native.VARIANT[desc.variant.value]
+    d.geometry_path = _native.GEO_PATH[desc.geometry_path.value]
+    d.dtype = dtype_code
+    d.layout = _native.LAYOUT[layout.kind.value]
+    d.lane_width = layout.lane_width if layout.kind is LayoutKind.LANE_INTERLEAVED else 1
+    d.n_elements = n
+    d.base_index = base
+    d.geometry, d.coefficients = geometry, coefficients
+    d.stiffness, d.load, d.error_key = stiffness, load, error_key
+    return d
+
+
+def _traffic(desc: KernelDescriptor, n: int) -> TrafficCounters:
+    ns = desc.element.n_shape
+    return TrafficCounters(n * desc.element.geometry_size, n * desc.problem.coefficient_size(desc.element),
+                           n * ns * ns, n * ns)
+
+
+def _check_match(desc: KernelDescriptor, batch) -> None:
+    etype, problem = coerce_element(batch.element_type), coerce_problem(batch.problem)
+    if etype is not desc.element or problem is not desc.problem:
+        raise ShapeMismatch(f"descriptor ({desc.element.value}, {desc.problem.value}) does not match "
+                            f"batch ({etype.value}, {problem.value})")
+
+
+_KIND_TEXT = {
+    _native.KIND_DEGENERATE: lambda det, tol: f"|det J| = {abs(det):.3e} <= {tol:.3e}",
+    _native.KIND_INVERTED: lambda det, tol: f"det J = {det:.3e} < 0",
+}
+
+
+def _raise_geometry(key: int, detail) -> None:
+    element, point, kind = _native.decode_error(key)
+    if kind == _native.KIND_PIPELINE_TIMEOUT:
+        raise NativeLibraryError("integration kernel pipeline timed out (internal error)")
+    det, tol = detail(element, point)
+    exc = DegenerateElement if kind == _native.KIND_DEGENERATE else InvertedElement
+    raise exc(_KIND_TEXT[kind](det, tol), element, point)
+
+
+def _device_error_detail(dd: _native.BatchDesc, local: int, point, stream) -> tuple[float, float]:
+    import torch
+
+    out = torch.empty(2, dtype=torch.float64, device="cuda")
+    lib = _native.load()
+    _native.check(lib.fek_error_detail(ctypes.byref(dd), local, -1 if point is None else point, out.data_ptr(),
+                                       stream), "fek_error_detail")
+    torch.cuda.current_stream().synchronize()
+    det, tol = out.tolist()
+    return det, tol
+
+
+# ---------------------------------------------------------------------------
+# device path
+# ---------------------------------------------------------------------------
+
+def _integrate_device(desc: KernelDescriptor, batch: DeviceBatch, out_layout, check: bool, base_index: int,
+                      out=None) -> BatchResult:
+    import torch
+
+    lib = _native.load()
+    n, ns = batch.n_elements, desc.element.n_shape
+    dev = batch.geometry_data.device
+    dtype_code = _native.DTYPE["float64" if batch.dtype == torch.float64 else "float32"]
+    if out is None:
+        A = torch.empty((n, ns, ns), dtype=batch.dtype, device=dev)
+        b = torch.empty((n, ns), dtype=batch.dtype, device=dev)
+    else:
+        A, b = out
+    err = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    dd = _desc_struct(desc, batch.layout, n, base_index, dtype_code, batch.geometry_data.data_ptr(),
+                      batch.coefficient_data.data_ptr(), A.data_ptr(), b.data_ptr(), err.data_ptr())
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream().cuda_stream
+        _native.check(lib.fek_integrate(ctypes.byref(dd), stream), "fek_integrate")
+        result = BatchResult(desc, n, A, b, _traffic(desc, n), coerce_layout(out_layout))
+        result.error_word = err
+        if check:
+            key = int(err.item()) & _native.NO_ERROR
+            if key != _native.NO_ERROR:
+                _raise_geometry(key, lambda e, q: _device_error_detail(dd, e - base_index, q, stream))
+    return result
+
+
+# ---------------------------------------------------------------------------
+# host path: chunked H2D -> kernel -> D2H pipeline inside libfek
+# ---------------------------------------------------------------------------
+
+_stream_cache: dict[int, list] = {}
+_stream_lock = threading.Lock()
+
+
+def _host_streams(device: int):
+    import torch
+
+    with _stream_lock:
+        if device not in _stream_cache:
+            _stream_cache[device] = [torch.cuda.Stream(device=device) for _ in range(HOST_STREAMS)]
+        return _stream_cache[device]
+
+
+def host_chunk_elements(n: int) -> int:
+    """Pipeline chunk: ~8+ chunks for big batches, multiple of the 128-element tile."""
+    chunk = max(16384, min(1 << 19, -(-n // 8)))
+    return -(-chunk // 128) * 128
+
+
+def _aligned_f64(a) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if a.ctypes.data % 16:
+        b = hostmem.empty(a.shape)
+        b[...] = a
+        return b
+    return a
+
+
+def _integrate_host(desc: KernelDescriptor, batch, out_layout, base_index: int) -> BatchResult:
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeLibraryError("no CUDA device available (there is no CPU fallback)")
+    lib = _native.load()
+    layout = coerce_layout(batch.layout)
+    n, ns = int(batch.n_elements), desc.element.n_shape
+    geo = _aligned_f64(batch.geometry_data)
+    cof = _aligned_f64(batch.coefficient_data)
+    A = hostmem.empty((n, ns, ns))
+    b = hostmem.empty((n, ns))
+    dd = _desc_struct(desc, layout, n, base_index, _native.DTYPE["float64"], geo.ctypes.data, cof.ctypes.data,
+                      A.ctypes.data, b.ctypes.data, 0)
+    device = torch.cuda.current_device()
+    streams = _host_streams(device)
+    chunk = host_chunk_elements(n)
+    ws_bytes = lib.fek_host_workspace_bytes(ctypes.byref(dd), len(streams), chunk)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
+    # the workspace came from torch's current stream; our streams must see it allocated
+    cur = torch.cuda.current_stream(device)
+    for s in streams:
+        s.wait_stream(cur)
+    handles = (ctypes.c_void_p * len(streams))(*[s.cuda_stream for s in streams])
+    key = ctypes.c_ulonglong(_native.NO_ERROR)
+    status = lib.fek_integrate_host(ctypes.byref(dd), ws.data_ptr(), ws_bytes, len(streams), handles, chunk,
+                                    ctypes.byref(key))
+    for s in streams:
+        cur.wait_stream(s)
+    if status == _native.ERR_GEOMETRY:
+        def detail(element, point):
+            # upload only the offending element (element-major row) and evaluate it on the GPU
+            w = layout.lane_width if layout.kind is LayoutKind.LANE_INTERLEAVED else 1
+            dsg = desc.element.geometry_size
+            blk, lane = divmod(element - base_index, w)
+            row = np.array(geo[blk * w * dsg + lane: blk * w * dsg + lane + dsg * w: w], dtype=np.float64)
+            g = torch.from_numpy(row).to(device)
+            d1 = _desc_struct(desc, ELEMENT_MAJOR, 1, element, 0, g.data_ptr(), 0, 0, 0, 0)
+            return _device_error_detail(d1, 0, point, cur.cuda_stream)
+
+        _raise_geometry(key.value, detail)
+    _native.check(status, "fek_integrate_host")
+    return BatchResult(desc, n, A, b, _traffic(desc, n), coerce_layout(out_layout))
+
+
+# ---------------------------------------------------------------------------
+# public entry point
+# ---------------------------------------------------------------------------
+
+def integrate_batch(desc, batch, out_layout: BatchLayout = ELEMENT_MAJOR, workers: int = 1, *,
+                    check: bool = True, base_index: int = 0, out=None) -> BatchResult:
+    """Integrate every element of ``batch`` with the kernel named by ``desc``.
+
+    Mirrors ``feklab.kernels.integrate_batch`` (``batched.py:536-606``).
+    Extra keyword-only knobs: ``check=False`` skips the device->host read of
+    the error word for device batches (``result.error_word`` holds it);
+    ``base_index`` offsets reported element indices (sharded batches);
+    ``out=(A, b)`` supplies preallocated device outputs.
+    """
+    desc = coerce_descriptor(desc)
+    _check_match(desc, batch)
+    if int(workers) < 1:
+        workers = 1
+    if isinstance(batch, DeviceBatch):
+        return _integrate_device(desc, batch, out_layout, check, base_index, out)
+    if _is_torch(getattr(batch, "geometry_data", None)):
+        raise TypeError("batches of torch tensors must be wrapped in DeviceBatch")
+    return _integrate_host(desc, batch, out_layout, base_index)
+
+
+def launch_config(desc, layout: BatchLayout, n: int, dtype: str = "float64") -> dict:
+    """Grid/block/smem/tile that ``fek_integrate`` uses for this case (no launch)."""
+    desc = coerce_descriptor(desc)
+    lib = _native.load()
+    dd = _desc_struct(desc, coerce_layout(layout), n, 0, _native.DTYPE[dtype], 0, 0, 0, 0, 0)
+    g, bl, sm, t = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _native.check(lib.fek_launch_config(ctypes.byref(dd), ctypes.byref(g), ctypes.byref(bl), ctypes.byref(sm),
+                                        ctypes.byref(t)), "fek_launch_config")
+    return {"grid": g.value, "block": bl.value, "smem_bytes": sm.value, "tile_elements": t.value}
