@@ -46,8 +46,10 @@ KernelEntry entry() {
 template <typename R, int ET, int PB>
 void fill_case(KernelEntry *table, int dtype) {
   table[kernel_index(dtype, ET, PB, QSS, GEO_GENERIC)] = entry<Traits<R, ET, PB, QSS, GEO_GENERIC>>();
+#ifndef FEK_QSS_ONLY  // (FEK_QSS_ONLY: fast single-kernel experiments only)
   table[kernel_index(dtype, ET, PB, SQS, GEO_GENERIC)] = entry<Traits<R, ET, PB, SQS, GEO_GENERIC>>();
   table[kernel_index(dtype, ET, PB, SSQ, GEO_GENERIC)] = entry<Traits<R, ET, PB, SSQ, GEO_GENERIC>>();
+#endif
   if constexpr (ET == TET) {
     // the reference's three geo_linear loop nests are one hoisted arithmetic
     // (bitwise equal in the reference itself): one kernel serves all three

@@ -97,7 +97,7 @@ __device__ __forceinline__ R degeneracy_tolerance(const R *X) {
       lo = fmin(lo, X[3 * v + i]);
     }
     const R span = hi - lo;
-    acc = fma(span, span, acc);
+    acc = (i == 0) ? span * span : acc + span * span;  // batched.py:145-147 rounding
   }
   const R scale = sqrt(acc);
   return R(1e-14) * (scale * scale * scale);
@@ -143,21 +143,24 @@ __device__ __forceinline__ int classify(R det, R tol) {
 }
 
 // sum_k c_k * x_k over compile-time coefficients, skipping zeros and using
-// +-1 as add/sub (the reference's _axpy_fixed, batched.py:119-133)
-template <typename R>
+// +-1 as add/sub (the reference's _axpy_fixed, batched.py:119-133).
+// EXACT = the reference's rounding: every product rounded, then summed left
+// to right (used for the Jacobian, whose entries are differences of absolute
+// coordinates and therefore ill-conditioned on fine meshes: matching the
+// reference's rounding there makes J bitwise equal to the reference's).
+// Otherwise products are fused into the running sum.
+template <typename R, bool EXACT = false>
 struct Lin {
   R acc;
   bool any = false;
-  template <int DUMMY = 0>
   __device__ __forceinline__ void add(double c, R x) {
     if (c == 0.0) return;
+    const R term = (c == 1.0) ? x : (c == -1.0 ? -x : R(c) * x);
     if (!any) {
-      acc = (c == 1.0) ? x : (c == -1.0 ? -x : R(c) * x);
+      acc = term;
       any = true;
-    } else if (c == 1.0) {
-      acc = acc + x;
-    } else if (c == -1.0) {
-      acc = acc - x;
+    } else if (EXACT || c == 1.0 || c == -1.0) {
+      acc = acc + term;
     } else {
       acc = fma(R(c), x, acc);
     }
@@ -167,22 +170,27 @@ struct Lin {
 
 #define FEK_CI(name, ic) constexpr int name = decltype(ic)::value
 
-// Per-point Jacobian at compile-time point Q: J[i][k] = sum_v ld[Q][v][k] X[v][i]
+// Jacobian entry J[i][K] at compile-time point Q: sum_v ld[Q][v][K] X[v][i]
+// with the reference's rounding (batched.py:193-207 via _axpy_fixed)
+template <int ET, int Q, int K, typename R>
+__device__ __forceinline__ R jac_entry(const R *X, int i) {
+  using S = Shape<ET>;
+  Lin<R, true> acc;
+  static_for<S::NV>([&](auto vc) {
+    FEK_CI(v, vc);
+    acc.add(S::ld(Q, v, K), X[3 * v + i]);
+  });
+  return acc.get();
+}
+
 template <int ET, int Q, typename R>
 __device__ __forceinline__ void point_jacobian(const R *X, R (&J)[3][3]) {
-  using S = Shape<ET>;
-  static_for<3>([&](auto ic) {
-    FEK_CI(i, ic);
-    static_for<3>([&](auto kc) {
-      FEK_CI(k, kc);
-      Lin<R> acc;
-      static_for<S::NV>([&](auto vc) {
-        FEK_CI(v, vc);
-        acc.add(S::ld(Q, v, k), X[3 * v + i]);
-      });
-      J[i][k] = acc.get();
-    });
-  });
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    J[i][0] = jac_entry<ET, Q, 0>(X, i);
+    J[i][1] = jac_entry<ET, Q, 1>(X, i);
+    J[i][2] = jac_entry<ET, Q, 2>(X, i);
+  }
 }
 
 // Global derivatives of shape function SF at point Q: g[i] = sum_k ld[Q][SF][k] inv[k][i]
@@ -300,6 +308,10 @@ struct PointData {
   __device__ __forceinline__ PointData(const R *X, R tol) {
     R J[3][3];
     point_jacobian<ET, Q>(X, J);
+    init(J, tol);
+  }
+  __device__ __forceinline__ PointData(const R (&J)[3][3], R tol) { init(J, tol); }
+  __device__ __forceinline__ void init(const R (&J)[3][3], R tol) {
     jac = invert3(J);
     kind = classify(jac.det, tol);
     constexpr R w = R(Shape<ET>::w(Q));
@@ -307,31 +319,11 @@ struct PointData {
   }
 };
 
-// ConvDiff t_s = vol * (C phi_s), phi_s = (val_s, g_s)
-template <typename R>
-__device__ __forceinline__ void cphi(const R *c, R val_s, const R (&g)[3], R vol, R (&t)[4]) {
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const R x = fma(c[4 * i + 1], g[0], fma(c[4 * i + 2], g[1], fma(c[4 * i + 3], g[2], c[4 * i] * val_s)));
-    t[i] = vol * x;
-  }
-}
-
-template <typename R>
-__device__ __forceinline__ R dot4(R val_r, const R (&g)[3], const R (&t)[4]) {
-  return fma(val_r, t[0], fma(g[0], t[1], fma(g[1], t[2], g[2] * t[3])));
-}
-
-template <typename R>
-__device__ __forceinline__ R load_term(const R *d, R val_r, const R (&g)[3]) {
-  return fma(d[0], val_r, fma(d[1], g[0], fma(d[2], g[1], d[3] * g[2])));
-}
-
 // Geometry source for the generic path: each call returns the element's
 // vertex coordinates, either from registers or re-read from the staged
-// shared-memory tile (keeps ~36 registers free on the FP64-bound prism path
-// and, for SQS/SSQ, makes the per-row / per-entry recomputation real work as
-// in the reference's loop skeletons).
+// shared-memory tile (keeps registers free on the FP64-bound prism path and,
+// for SQS/SSQ, makes the per-row / per-entry recomputation real work as in
+// the reference's loop skeletons).
 template <typename R, int DS>
 struct RegGeometry {
   const R (&X)[DS];
@@ -348,6 +340,81 @@ struct SmemGeometry {
   int width;
   __device__ __forceinline__ void fetch(R (&out)[DS]) const { RowIO<R, DS>::load(tile, lane, width, out); }
 };
+
+// Visit every quadrature point with its point data, computing each DISTINCT
+// Jacobian column once.  Tets: J is point-independent.  Prisms (q = 2t + z):
+// columns 0/1 depend only on the zeta level z, column 2 only on the triangle
+// point t (refelem.py:145-155).  The reference recomputes J per point; the
+// values are bitwise the same (identical operations on identical operands).
+// Points are visited z-major for prisms (accumulation order is free: A is
+// not bitwise-matched, only J is).
+template <typename R, int ET, class Geo, class F>
+__device__ __forceinline__ void for_each_point(const Geo &geo, R tol, F &&f) {
+  constexpr int DSG = 3 * Shape<ET>::NV;
+  if constexpr (ET == TET) {
+    R X[DSG];
+    geo.fetch(X);
+    R J[3][3];
+    point_jacobian<TET, 0>(X, J);
+    const PointData<TET, 0, R> pd(J, tol);  // w_q and J are the same at all 4 points
+    static_for<4>([&](auto qc) {
+      FEK_CI(Q, qc);
+      f(std::integral_constant<int, Q>{}, pd);
+    });
+  } else {
+    R J2[3][3];  // [t][i]
+    R J01[2][3][2];  // [z][i][k]
+    {
+      R X[DSG];
+      geo.fetch(X);
+      static_for<3>([&](auto tc) {
+        FEK_CI(t, tc);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) J2[t][i] = jac_entry<PRISM, 2 * t, 2>(X, i);
+      });
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        J01[0][i][0] = jac_entry<PRISM, 0, 0>(X, i);
+        J01[0][i][1] = jac_entry<PRISM, 0, 1>(X, i);
+        J01[1][i][0] = jac_entry<PRISM, 1, 0>(X, i);
+        J01[1][i][1] = jac_entry<PRISM, 1, 1>(X, i);
+      }
+    }
+    static_for<2>([&](auto zc) {
+      FEK_CI(z, zc);
+      static_for<3>([&](auto tc) {
+        FEK_CI(t, tc);
+        constexpr int Q = 2 * t + z;
+        const R J[3][3] = {{J01[z][0][0], J01[z][0][1], J2[t][0]},
+                           {J01[z][1][0], J01[z][1][1], J2[t][1]},
+                           {J01[z][2][0], J01[z][2][1], J2[t][2]}};
+        const PointData<PRISM, Q, R> pd(J, tol);
+        f(std::integral_constant<int, Q>{}, pd);
+      });
+    });
+  }
+}
+
+// ConvDiff t_s = vol * (C phi_s), phi_s = (val_s, g_s)
+template <typename R>
+__device__ __forceinline__ void cphi(const R *c, R val_s, const R (&g)[3], R vol, R (&t)[4]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const R x = fma(c[4 * i + 1], g[0], fma(c[4 * i + 2], g[1], fma(c[4 * i + 3], g[2], c[4 * i] * val_s)));
+    t[i] = vol * x;
+  }
+}
+
+// acc + (val_r, g_r) . t, fused into the accumulator (4 FMA, no extra add)
+template <typename R>
+__device__ __forceinline__ R acc_dot4(R acc, R val_r, const R (&g)[3], const R (&t)[4]) {
+  return fma(g[2], t[3], fma(g[1], t[2], fma(g[0], t[1], fma(val_r, t[0], acc))));
+}
+
+template <typename R>
+__device__ __forceinline__ R load_term(const R *d, R val_r, const R (&g)[3]) {
+  return fma(d[0], val_r, fma(d[1], g[0], fma(d[2], g[1], d[3] * g[2])));
+}
 
 template <typename R, int ET, int PB, int VAR, class Geo>
 __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef, R tol,
@@ -370,11 +437,8 @@ __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef,
   for (int i = 0; i < NS; ++i) B[i] = R(0);
 
   if constexpr (VAR == QSS) {
-    static_for<NQ>([&](auto qc) {
+    for_each_point<R, ET>(geo, tol, [&](auto qc, const auto &pd) {
       FEK_CI(Q, qc);
-      R X[DSG];
-      geo.fetch(X);
-      const PointData<ET, Q, R> pd(X, tol);
       note(pd.kind, Q);
       R g[NS][3];
       all_grads<ET, Q>(pd.jac, g);
@@ -396,7 +460,7 @@ __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef,
           cphi(coef, R(S::val(Q, s)), g[s], pd.vol, t);
           static_for<NS>([&](auto rc) {
             FEK_CI(r, rc);
-            A[NS * r + s] += dot4(R(S::val(Q, r)), g[r], t);
+            A[NS * r + s] = acc_dot4(A[NS * r + s], R(S::val(Q, r)), g[r], t);
           });
         });
         static_for<NS>([&](auto rc) {
@@ -434,7 +498,7 @@ __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef,
             u[j] = pd.vol * fma(coef[4 + j], g[r][0], fma(coef[8 + j], g[r][1], fma(coef[12 + j], g[r][2], coef[j] * vr)));
           static_for<NS>([&](auto sc) {
             FEK_CI(s, sc);
-            A[NS * r + s] += dot4(R(S::val(Q, s)), g[s], u);
+            A[NS * r + s] = acc_dot4(A[NS * r + s], R(S::val(Q, s)), g[s], u);
           });
           B[r] = fma(pd.vol, load_term(coef + 16, vr, g[r]), B[r]);
         }
@@ -466,7 +530,7 @@ __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef,
             } else {
               R t[4];
               cphi(coef, vs, gs, pd.vol, t);
-              A[NS * r + s] += dot4(vr, gr, t);
+              A[NS * r + s] = acc_dot4(A[NS * r + s], vr, gr, t);
               if constexpr (r == s) B[r] = fma(pd.vol, load_term(coef + 16, vr, gr), B[r]);
             }
           });
