@@ -314,7 +314,10 @@ def run_ours(args) -> int:
     e2e = None
     if not args.no_e2e:
         e2e_steps = max(1, min(args.steps, 10))
-        integrate_batch(desc, host_batch)  # warm (pinned result blocks, streams, workspace)
+        # warm exactly like the timed loop: two results alive at once, so the
+        # caching pinned-host allocator holds both result blocks before timing
+        res = integrate_batch(desc, host_batch, base_index=rank * n)
+        res = integrate_batch(desc, host_batch, base_index=rank * n)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()

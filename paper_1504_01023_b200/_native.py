@@ -15,6 +15,8 @@ import threading
 from .errors import NativeLibraryError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfek.so")
+if os.environ.get("FEK_LIB_OVERRIDE"):  # kernel-tuning experiments only
+    LIB_PATH = os.path.abspath(os.environ["FEK_LIB_OVERRIDE"])
 HEADER_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "fek.h")
 
 ABI_VERSION = 1

@@ -111,6 +111,47 @@ struct Jac {
   R det;
 };
 
+// 1/x: hardware approximation + two Newton steps (~1 ulp; no slow-path
+// branch).  x = 0 / denormal only happens for degenerate elements, which are
+// reported and whose outputs are discarded.
+__device__ __forceinline__ double recip(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ float recip(float x) { return 1.0f / x; }
+
+template <typename R>
+__device__ __forceinline__ R det3(const R (&J)[3][3]) {
+  const R k00 = fma(J[1][1], J[2][2], -(J[1][2] * J[2][1]));
+  const R k01 = fma(J[1][2], J[2][0], -(J[1][0] * J[2][2]));
+  const R k02 = fma(J[1][0], J[2][1], -(J[1][1] * J[2][0]));
+  return fma(J[0][0], k00, fma(J[0][1], k01, J[0][2] * k02));
+}
+
+// inverse from a precomputed determinant and its reciprocal
+template <typename R>
+__device__ __forceinline__ Jac<R> invert3_with(const R (&J)[3][3], R det, R r) {
+  const R a = J[0][0], b = J[0][1], c = J[0][2];
+  const R d = J[1][0], e = J[1][1], f = J[1][2];
+  const R g = J[2][0], h = J[2][1], i = J[2][2];
+  Jac<R> out;
+  out.det = det;
+  out.inv[0][0] = fma(e, i, -(f * h)) * r;
+  out.inv[0][1] = fma(c, h, -(b * i)) * r;
+  out.inv[0][2] = fma(b, f, -(c * e)) * r;
+  out.inv[1][0] = fma(f, g, -(d * i)) * r;
+  out.inv[1][1] = fma(a, i, -(c * g)) * r;
+  out.inv[1][2] = fma(c, d, -(a * f)) * r;
+  out.inv[2][0] = fma(d, h, -(e * g)) * r;
+  out.inv[2][1] = fma(b, g, -(a * h)) * r;
+  out.inv[2][2] = fma(a, e, -(b * d)) * r;
+  return out;
+}
+
 template <typename R>
 __device__ __forceinline__ Jac<R> invert3(const R (&J)[3][3]) {
   const R a = J[0][0], b = J[0][1], c = J[0][2];
@@ -121,7 +162,7 @@ __device__ __forceinline__ Jac<R> invert3(const R (&J)[3][3]) {
   const R k02 = fma(d, h, -(e * g));
   Jac<R> out;
   out.det = fma(a, k00, fma(b, k01, c * k02));
-  const R r = R(1) / out.det;
+  const R r = recip(out.det);
   out.inv[0][0] = k00 * r;
   out.inv[0][1] = fma(c, h, -(b * i)) * r;
   out.inv[0][2] = fma(b, f, -(c * e)) * r;
@@ -311,6 +352,12 @@ struct PointData {
     init(J, tol);
   }
   __device__ __forceinline__ PointData(const R (&J)[3][3], R tol) { init(J, tol); }
+  __device__ __forceinline__ PointData(const R (&J)[3][3], R det, R r, R tol) {
+    jac = invert3_with(J, det, r);
+    kind = classify(det, tol);
+    constexpr R w = R(Shape<ET>::w(Q));
+    vol = det * w;
+  }
   __device__ __forceinline__ void init(const R (&J)[3][3], R tol) {
     jac = invert3(J);
     kind = classify(jac.det, tol);
@@ -416,8 +463,18 @@ __device__ __forceinline__ R load_term(const R *d, R val_r, const R (&g)[3]) {
   return fma(d[0], val_r, fma(d[1], g[0], fma(d[2], g[1], d[3] * g[2])));
 }
 
-template <typename R, int ET, int PB, int VAR, class Geo>
-__device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef, R tol,
+// Source of the load coefficients d (ConvDiff).
+template <typename R>
+struct RegLoad {
+  const R *d;
+  __device__ __forceinline__ void fetch(R (&out)[4]) const {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) out[k] = d[k];
+  }
+};
+
+template <typename R, int ET, int PB, int VAR, class Geo, class Load>
+__device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef, const Load &load, R tol,
                                                   R (&A)[Shape<ET>::NS * Shape<ET>::NS],
                                                   R (&B)[Shape<ET>::NS], int &kind, int &kind_point) {
   using S = Shape<ET>;
@@ -463,9 +520,14 @@ __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef,
             A[NS * r + s] = acc_dot4(A[NS * r + s], R(S::val(Q, r)), g[r], t);
           });
         });
+        // load vector as a 7th column: B_r += phi_r . (vol d)
+        R tb[4];
+        load.fetch(tb);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) tb[k] = pd.vol * tb[k];
         static_for<NS>([&](auto rc) {
           FEK_CI(r, rc);
-          B[r] = fma(pd.vol, load_term(coef + 16, R(S::val(Q, r)), g[r]), B[r]);
+          B[r] = acc_dot4(B[r], R(S::val(Q, r)), g[r], tb);
         });
       }
     });

@@ -1,26 +1,31 @@
 // fek_kernel.cuh -- the persistent, TMA-pipelined integration kernel.
 //
-// One CTA = 128 threads = one tile of TILE = 128 elements at a time (one
-// element per thread).  CTAs are persistent (grid = SMs x resident CTAs) and
-// walk tiles t = blockIdx.x + k*gridDim.x.  Per tile:
+// One CTA = 128 threads (4 warps) = one tile of TILE = 128 elements at a
+// time, one element per thread.  CTAs are persistent (grid = SMs x resident
+// CTAs) and walk tiles t = blockIdx.x + i*gridDim.x.  Per tile i:
 //
 //   1. the tile's geometry and coefficient byte ranges (contiguous in both
 //      the element-major and the lane-interleaved layout, because TILE is a
 //      multiple of every lane width) arrive by 1-D TMA bulk copies into stage
-//      k % STAGES, completion counted on that stage's mbarrier;
+//      i % STAGES; completion is counted on full[stage] (arrival + bytes);
 //   2. each thread pulls its element's rows into registers (conflict-free
-//      rotated 16-byte reads, fek_device.cuh) -- or, for the FP64-bound
-//      prism path, only the coefficients, re-reading vertex coordinates from
-//      the tile per quadrature point;
-//   3. once the stage is consumed, thread 0 refills it with tile k+STAGES;
+//      rotated 16-byte reads, fek_device.cuh) -- or, on the FP64-bound prism
+//      path, only the coefficients, re-reading the vertex coordinates from
+//      the staged tile when the Jacobian columns are formed;
+//   3. once every thread is done with the stage (CTA barrier), thread 0
+//      refills it with tile i + STAGES;
 //   4. the element math runs in registers (fek_element.cuh);
 //   5. A and b rows are written to one shared output tile (the exact global
-//      byte image) and leave the SM as two TMA bulk stores, i.e. full-line
-//      coalesced writes; the next tile waits for the store to have READ the
-//      tile (bulk_wait_read) before overwriting it.
+//      byte image) and leave the SM as two TMA bulk stores (full-line
+//      coalesced writes); the next tile waits until those stores have READ
+//      the tile (bulk_wait_read) before overwriting it.
 //
-// Geometry failures are reduced to one 64-bit key per element and merged with
-// a single atomicMin into the caller's error word.
+// The barriers keep the four warps in step.  A warp-decoupled variant
+// (per-warp mbarrier release + per-warp output slices) was measured slower on
+// every case -- up to 12% on the FP64-bound prism kernel, whose ~60 KB of
+// unrolled SASS thrashes the instruction cache once warps drift apart
+// (DESIGN.md section 6).  Geometry failures become one 64-bit key per element,
+// merged with atomicMin into the caller's error word.
 #pragma once
 
 #include "fek_element.cuh"
@@ -53,15 +58,19 @@ struct Traits {
   // the staged tile instead of pinning 18 reals in registers
   static constexpr bool LAZY_X = (GEO == GEO_GENERIC) && (ET == PRISM || VAR != QSS);
   // stages / resident CTAs: memory-bound tets keep >= 64 KB of loads in
-  // flight per SM; prisms trade stages for resident warps (FP64 latency)
-  static constexpr int STAGES = (ET == TET && PB == POISSON) ? 3 : (LAZY_X && PB == CONV_DIFF ? 1 : 2);
+  // flight per SM; the FP64-bound prism CDR kernel needs its shared memory
+  // for two resident CTAs (8 warps) more than for a second stage
+  static constexpr int STAGES = (ET == TET && PB == POISSON) ? 3 : ((LAZY_X && PB == CONV_DIFF) ? 1 : 2);
   static constexpr int MIN_BLOCKS = (ET == TET && PB == POISSON) ? 3 : 2;
   static constexpr unsigned GEO_TILE_BYTES = TILE * DSG * sizeof(R);
   static constexpr unsigned COEF_TILE_BYTES = TILE * DSC * sizeof(R);
-  static constexpr unsigned STAGE_BYTES = GEO_TILE_BYTES + COEF_TILE_BYTES;
   static constexpr unsigned OUT_A_BYTES = TILE * NA * sizeof(R);
   static constexpr unsigned OUT_B_BYTES = TILE * NS * sizeof(R);
-  static constexpr unsigned BAR_OFFSET = STAGES * STAGE_BYTES + OUT_A_BYTES + OUT_B_BYTES;
+  static constexpr unsigned GEO_OFFSET = 0;
+  static constexpr unsigned COEF_OFFSET = STAGES * GEO_TILE_BYTES;
+  static constexpr unsigned OUT_A_OFFSET = COEF_OFFSET + STAGES * COEF_TILE_BYTES;
+  static constexpr unsigned OUT_B_OFFSET = OUT_A_OFFSET + OUT_A_BYTES;
+  static constexpr unsigned BAR_OFFSET = OUT_B_OFFSET + OUT_B_BYTES;
   static constexpr unsigned SMEM_BYTES = BAR_OFFSET + 8 * STAGES;
   static_assert(GEO_TILE_BYTES % 16 == 0 && COEF_TILE_BYTES % 16 == 0, "tile alignment");
   static_assert(OUT_A_BYTES % 16 == 0 && OUT_B_BYTES % 16 == 0, "tile alignment");
@@ -81,58 +90,61 @@ __device__ __forceinline__ void copy_tail(uint32_t dst, const char *src, unsigne
 }
 
 template <class K>
-__device__ __forceinline__ void issue_tile(const LaunchParams &p, long long t, uint32_t geo_dst, uint32_t coef_dst,
-                                           uint32_t bar, uint64_t policy) {
+struct Pipe {
   using R = typename K::R;
-  const long long e0 = t * K::TILE;
-  const int count = static_cast<int>(min(static_cast<long long>(K::TILE), p.n - e0));
-  const unsigned gb = tile_bytes(count, p.lane_width, K::DSG, sizeof(R));
-  const unsigned cb = tile_bytes(count, p.lane_width, K::DSC, sizeof(R));
-  const char *gsrc = static_cast<const char *>(p.geometry) + e0 * K::DSG * sizeof(R);
-  const char *csrc = static_cast<const char *>(p.coefficients) + e0 * K::DSC * sizeof(R);
-  // sub-16-byte tails first (plain stores, ordered before the arrive's
-  // release), then arm the barrier with the bulk byte count, then the bulk
-  // copies: the phase completes when the arrival and all bytes are in
-  copy_tail(geo_dst, gsrc, gb);
-  copy_tail(coef_dst, csrc, cb);
-  mbar_arrive_expect_tx(bar, (gb & ~15u) + (cb & ~15u));
-  if (gb & ~15u) bulk_load(geo_dst, gsrc, gb & ~15u, bar, policy);
-  if (cb & ~15u) bulk_load(coef_dst, csrc, cb & ~15u, bar, policy);
-}
+  uint32_t sbase;
+  long long tiles;
+  uint64_t policy;
+
+  __device__ __forceinline__ uint32_t geo(int s) const { return sbase + K::GEO_OFFSET + s * K::GEO_TILE_BYTES; }
+  __device__ __forceinline__ uint32_t coef(int s) const { return sbase + K::COEF_OFFSET + s * K::COEF_TILE_BYTES; }
+  __device__ __forceinline__ uint32_t full(int s) const { return sbase + K::BAR_OFFSET + 8 * s; }
+
+  // thread 0: stage tile t into stage s.  Sub-16-byte tails first (plain
+  // stores, ordered before the arrive's release), then arm the barrier with
+  // the bulk byte count, then the bulk copies: the phase completes when the
+  // arrival and all transaction bytes are in.
+  __device__ __forceinline__ void issue(const LaunchParams &p, long long t, int s) const {
+    if (t >= tiles) return;
+    const long long e0 = t * K::TILE;
+    const int count = static_cast<int>(min(static_cast<long long>(K::TILE), p.n - e0));
+    const unsigned gb = tile_bytes(count, p.lane_width, K::DSG, sizeof(R));
+    const unsigned cb = tile_bytes(count, p.lane_width, K::DSC, sizeof(R));
+    const char *gsrc = static_cast<const char *>(p.geometry) + e0 * K::DSG * sizeof(R);
+    const char *csrc = static_cast<const char *>(p.coefficients) + e0 * K::DSC * sizeof(R);
+    copy_tail(geo(s), gsrc, gb);
+    copy_tail(coef(s), csrc, cb);
+    mbar_arrive_expect_tx(full(s), (gb & ~15u) + (cb & ~15u));
+    if (gb & ~15u) bulk_load(geo(s), gsrc, gb & ~15u, full(s), policy);
+    if (cb & ~15u) bulk_load(coef(s), csrc, cb & ~15u, full(s), policy);
+  }
+};
 
 template <class K>
 __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(const LaunchParams p) {
   using R = typename K::R;
   extern __shared__ __align__(128) unsigned char smem[];
-  const uint32_t sbase = smem_u32(smem);
   const int tid = threadIdx.x;
-  const long long tiles = (p.n + K::TILE - 1) / K::TILE;
-  const uint32_t bars = sbase + K::BAR_OFFSET;
-  const uint32_t out_a = sbase + K::STAGES * K::STAGE_BYTES;
-  const uint32_t out_b = out_a + K::OUT_A_BYTES;
-  auto geo_stage = [&](int s) { return sbase + s * K::STAGE_BYTES; };
-  auto coef_stage = [&](int s) { return sbase + s * K::STAGE_BYTES + K::GEO_TILE_BYTES; };
-
-  uint64_t policy = 0;
+  Pipe<K> pipe;
+  pipe.sbase = smem_u32(smem);
+  pipe.tiles = (p.n + K::TILE - 1) / K::TILE;
+  pipe.policy = 0;
+  const uint32_t out_a = pipe.sbase + K::OUT_A_OFFSET;
+  const uint32_t out_b = pipe.sbase + K::OUT_B_OFFSET;
   if (tid == 0) {
-    policy = policy_evict_first();
-    for (int s = 0; s < K::STAGES; ++s) mbar_init(bars + 8 * s, 1);
+    pipe.policy = policy_evict_first();
+    for (int s = 0; s < K::STAGES; ++s) mbar_init(pipe.full(s), 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0) {
-    for (int s = 0; s < K::STAGES; ++s) {
-      const long long t = blockIdx.x + static_cast<long long>(s) * gridDim.x;
-      if (t < tiles) issue_tile<K>(p, t, geo_stage(s), coef_stage(s), bars + 8 * s, policy);
-    }
-  }
+  if (tid == 0)
+    for (int s = 0; s < K::STAGES; ++s) pipe.issue(p, blockIdx.x + static_cast<long long>(s) * gridDim.x, s);
 
-  int k = 0;
-  for (long long t = blockIdx.x; t < tiles; t += gridDim.x, ++k) {
-    const int s = k % K::STAGES;
-    const uint32_t parity = (k / K::STAGES) & 1;
-    const bool landed = mbar_wait(bars + 8 * s, parity);
-    if (__syncthreads_or(!landed)) {  // uniform bail-out instead of a hang
+  int i = 0;
+  for (long long t = blockIdx.x; t < pipe.tiles; t += gridDim.x, ++i) {
+    const int s = i % K::STAGES;
+    const bool landed = mbar_wait(pipe.full(s), (i / K::STAGES) & 1);
+    if (__syncthreads_or(!landed)) {
       if (tid == 0) atomicMin(p.error_key, static_cast<unsigned long long>(KIND_PIPELINE_TIMEOUT));
       return;
     }
@@ -140,7 +152,7 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
     const int count = static_cast<int>(min(static_cast<long long>(K::TILE), p.n - e0));
     const bool active = tid < count;
     const long long e_abs = p.base + e0 + tid;
-
+    const long long tn = t + static_cast<long long>(K::STAGES) * gridDim.x;
     R C[K::DSC];
     R A[K::NA];
     R B[K::NS];
@@ -148,40 +160,35 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
     if constexpr (!K::LAZY_X) {
       R X[K::DSG];
       if (active) {
-        RowIO<R, K::DSG>::load(geo_stage(s), tid, p.lane_width, X);
-        RowIO<R, K::DSC>::load(coef_stage(s), tid, p.lane_width, C);
+        RowIO<R, K::DSG>::load(pipe.geo(s), tid, p.lane_width, X);
+        RowIO<R, K::DSC>::load(pipe.coef(s), tid, p.lane_width, C);
       }
-      __syncthreads();  // stage s consumed by every thread
-      if (tid == 0) {
-        const long long tn = t + static_cast<long long>(K::STAGES) * gridDim.x;
-        if (tn < tiles) issue_tile<K>(p, tn, geo_stage(s), coef_stage(s), bars + 8 * s, policy);
-      }
+      __syncthreads();
+      if (tid == 0) pipe.issue(p, tn, s);
       if (active) {
         if constexpr (K::GEO == GEO_LINEAR) {
           integrate_tet_linear<R, K::PB>(X, C, A, B, kind);
         } else {
           const R tol = degeneracy_tolerance<R, K::NV>(X);
-          integrate_generic<R, K::ET, K::PB, K::VAR>(RegGeometry<R, K::DSG>{X}, C, tol, A, B, kind, kind_point);
+          integrate_generic<R, K::ET, K::PB, K::VAR>(RegGeometry<R, K::DSG>{X}, C, RegLoad<R>{C + (K::DSC >= 20 ? 16 : 0)},
+                                                     tol, A, B, kind, kind_point);
         }
       }
     } else {
       if (active) {
-        RowIO<R, K::DSC>::load(coef_stage(s), tid, p.lane_width, C);
-        const SmemGeometry<R, K::DSG> geo{geo_stage(s), tid, p.lane_width};
+        RowIO<R, K::DSC>::load(pipe.coef(s), tid, p.lane_width, C);
+        const SmemGeometry<R, K::DSG> geo{pipe.geo(s), tid, p.lane_width};
         R X[K::DSG];
         geo.fetch(X);
         const R tol = degeneracy_tolerance<R, K::NV>(X);
-        integrate_generic<R, K::ET, K::PB, K::VAR>(geo, C, tol, A, B, kind, kind_point);
+        integrate_generic<R, K::ET, K::PB, K::VAR>(geo, C, RegLoad<R>{C + (K::DSC >= 20 ? 16 : 0)}, tol, A, B, kind,
+                                                   kind_point);
       }
-      __syncthreads();  // stage s consumed
-      if (tid == 0) {
-        const long long tn = t + static_cast<long long>(K::STAGES) * gridDim.x;
-        if (tn < tiles) issue_tile<K>(p, tn, geo_stage(s), coef_stage(s), bars + 8 * s, policy);
-      }
+      __syncthreads();
+      if (tid == 0) pipe.issue(p, tn, s);
     }
     if (kind) atomicMin(p.error_key, make_error_key(e_abs, kind_point, kind));
-
-    if (tid == 0) bulk_wait_read<0>();  // previous tile's stores have read the out tile
+    if (tid == 0) bulk_wait_read<0>();
     __syncthreads();
     if (active) {
       RowIO<R, K::NA>::store_major(out_a, tid, A);
@@ -190,17 +197,15 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
-      const unsigned ab = count * K::NA * sizeof(R);
-      const unsigned bb = count * K::NS * sizeof(R);
+      const unsigned ab = count * K::NA * sizeof(R), bb = count * K::NS * sizeof(R);
       char *ga = static_cast<char *>(p.stiffness) + e0 * K::NA * sizeof(R);
       char *gb = static_cast<char *>(p.load) + e0 * K::NS * sizeof(R);
       const unsigned ab16 = ab & ~15u, bb16 = bb & ~15u;
       if (ab16) bulk_store(ga, out_a, ab16);
       if (bb16) bulk_store(gb, out_b, bb16);
       bulk_commit();
-      // fp32 prism load rows (24 B) with an odd count leave an 8-byte tail
-      for (unsigned i = ab16; i < ab; i += 4) *reinterpret_cast<uint32_t *>(ga + i) = lds32(out_a + i);
-      for (unsigned i = bb16; i < bb; i += 4) *reinterpret_cast<uint32_t *>(gb + i) = lds32(out_b + i);
+      for (unsigned k = ab16; k < ab; k += 4) *reinterpret_cast<uint32_t *>(ga + k) = lds32(out_a + k);
+      for (unsigned k = bb16; k < bb; k += 4) *reinterpret_cast<uint32_t *>(gb + k) = lds32(out_b + k);
     }
   }
   if (tid == 0) bulk_wait_all<0>();
