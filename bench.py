@@ -242,7 +242,8 @@ def measure_case(key, steps, warmup, variant="qss"):
         "elements": n, "descriptor": desc.short_name(), "dtype": "f32" if fp32 else "f64",
         "value": n / (ms / 1e3), "unit": UNIT, "ms_per_launch": ms, "ms_min": float(np.min(per)),
         "buffer_sets": sets,
-        "roofline": case_roofline(et, pb, n, ms / 1e3, rb),
+        "roofline": dict(case_roofline(et, pb, n, ms / 1e3, rb),
+                         traffic=load_profile_traffic(f"{desc.short_name()}_{'f32' if fp32 else 'f64'}")),
         "parity": {"max_rel_frobenius": err, "elements_checked": cnt, "tolerance": tol, "pass": err <= tol,
                    "against": "numpy oracle (bitwise-pinned restatement of the reference)"},
     }
@@ -295,7 +296,7 @@ def run_ours(args) -> int:
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local, period=0.0005)
     per, total_ms = time_launches([launcher], args.steps, args.warmup, sampler)
     key = launcher.error_key()
     if key != 0xFFFFFFFFFFFFFFFF:
@@ -308,7 +309,17 @@ def run_ours(args) -> int:
     step_ms, launch_ms = t.tolist()
     value = world * n / (step_ms / 1e3)
     clocks = sampler.summary()
-    reject = clocks_rejected(clocks)
+    # the timed region is only a few ms: also sample a ~1 s sustained run of
+    # the same launches so the clock record has enough samples under load
+    sustained = ClockSampler(local, period=0.005)
+    with sustained:
+        t_end = time.time() + 1.0
+        while time.time() < t_end:
+            for _ in range(20):
+                launcher()
+            torch.cuda.synchronize()
+    clocks["sustained_1s"] = sustained.summary()
+    reject = clocks_rejected(clocks) or clocks_rejected(clocks["sustained_1s"])
 
     # ---- end-to-end through the public API on host buffers ----
     e2e = None

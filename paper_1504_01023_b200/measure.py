@@ -10,9 +10,10 @@ Roofline definitions:
   ``frac`` = roof time / measured time.
 
 HBM peak: ``MEASURED_PEAKS.json`` ``hbm_gbs`` (driver-measured copy bandwidth
-on this pool's B200s), else the profiling guide's 6650 GB/s fallback.  FP64
-peak: measured on the box by ``fek_probe`` when available, else the nominal
-148 SMs x 64 DFMA/clk x 2 x 1.965 GHz = 37.2 TFLOP/s.
+on this pool's B200s), else the profiling guide's 6650 GB/s fallback.  FP64 /
+FP32 peaks: measured on the box by ``tools/probe_peaks.py`` (independent
+DFMA/FFMA chains on all SMs; ``profiles/peaks_r01.json``), else the nominal
+148 SMs x 64 DFMA/clk x 2 x 1.965 GHz = 37.2 TFLOP/s (x2 for fp32).
 """
 
 from __future__ import annotations
@@ -41,13 +42,23 @@ def hbm_peak() -> tuple[float, str]:
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def case_roofline(element: ElementType, problem: ProblemClass, n: int, seconds: float, real_bytes: int = 8,
-                  fp64_tflops: float | None = None, fp64_source: str = "nominal") -> dict:
+def flop_peak(real_bytes: int = 8) -> tuple[float, str]:
+    """Measured FMA-pipe peak (tools/probe_peaks.py -> profiles/peaks_r01.json), else nominal."""
+    key = "fp64_tflops_best" if real_bytes == 8 else "fp32_tflops_best"
+    path = os.path.join(ROOT, "profiles", "peaks_r01.json")
+    try:
+        with open(path) as fh:
+            val = float(json.load(fh)[key])
+        return val, f"measured (profiles/peaks_r01.json {key}, DFMA/FFMA chains on 148 SMs)"
+    except Exception:
+        nominal = NOMINAL_FP64_TFLOPS * (1 if real_bytes == 8 else 2)
+        return nominal, "nominal (148 SM x 64 DFMA/clk x 2 x 1.965 GHz; x2 for fp32)"
+
+
+def case_roofline(element: ElementType, problem: ProblemClass, n: int, seconds: float, real_bytes: int = 8) -> dict:
     """Roofline record for n elements integrated in ``seconds`` (one launch)."""
     hbm, hbm_src = hbm_peak()
-    peak_f = fp64_tflops or NOMINAL_FP64_TFLOPS
-    if real_bytes == 4:
-        peak_f = peak_f * 2.0  # FP32 non-tensor rate is 2x FP64 on B200
+    peak_f, fp64_source = flop_peak(real_bytes)
     by = algorithmic_bytes(element, problem, real_bytes) * n
     fl = algorithmic_flops(element, problem) * n
     t_mem = by / (hbm * 1e9)

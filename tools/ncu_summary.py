@@ -1,0 +1,96 @@
+#!/usr/bin/env python
+"""Summarise ncu reports into profiles/ncu_summary.json (+ a markdown table).
+
+    python tools/ncu_summary.py TAG=gpurun_out/prof_C2.ncu-rep ... [--md profiles/ncu_r01.md]
+
+Run here (no GPU): reads the .ncu-rep files with `ncu -i --page raw --csv`.
+The JSON is keyed by kernel tag (descriptor_dtype), which bench.py uses to
+fill roofline.traffic (dram bytes per launch).
+"""
+import argparse
+import csv
+import io
+import json
+import os
+import subprocess
+
+METRICS = {
+    "duration_us": ("gpu__time_duration.sum", 1e-3),
+    "dram_read_bytes": ("dram__bytes_read.sum", None),
+    "dram_write_bytes": ("dram__bytes_write.sum", None),
+    "dram_pct_peak": ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", None),
+    "fp64_pipe_pct": ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", None),
+    "fma_pipe_pct": ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", None),
+    "warps_active_pct": ("sm__warps_active.avg.pct_of_peak_sustained_active", None),
+    "registers": ("launch__registers_per_thread", None),
+    "grid": ("launch__grid_size", None),
+    "smem_bank_conflicts": ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", None),
+    "smem_wavefronts": ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", None),
+    "local_loads": ("smsp__sass_inst_executed_op_local_ld.sum", None),
+    "inst_executed": ("smsp__inst_executed.sum", None),
+    "sm_clock_ghz": ("sm__cycles_elapsed.avg.per_second", None),
+}
+UNITS = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "ms": 1e3, "us": 1.0, "ns": 1e-3}
+
+
+def read(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    rec = {"kernel": vals[hdr.index("Kernel Name")]}
+    for key, (metric, _) in METRICS.items():
+        if metric not in hdr:
+            continue
+        i = hdr.index(metric)
+        try:
+            v = float(vals[i].replace(",", ""))
+        except ValueError:
+            continue
+        u = units[i]
+        if key.endswith("_bytes") and u in UNITS:
+            v *= UNITS[u]
+        if key == "duration_us" and u in UNITS:
+            v *= UNITS[u]
+        rec[key] = v
+    stalls = {}
+    for i, h in enumerate(hdr):
+        if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("_not_issued"):
+            try:
+                stalls[h[len("smsp__pcsamp_warps_issue_stalled_"):]] = float(vals[i])
+            except ValueError:
+                pass
+    tot = sum(stalls.values()) or 1.0
+    rec["stall_pct"] = {k: round(100 * v / tot, 1) for k, v in sorted(stalls.items(), key=lambda kv: -kv[1])[:8]}
+    rec["dram_bytes_per_launch"] = rec.get("dram_read_bytes", 0) + rec.get("dram_write_bytes", 0)
+    return rec
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("reports", nargs="+", help="TAG=path.ncu-rep")
+    ap.add_argument("--out", default="profiles/ncu_summary.json")
+    ap.add_argument("--md", default=None)
+    args = ap.parse_args()
+    data = {}
+    if os.path.exists(args.out):
+        data = json.load(open(args.out))
+    for item in args.reports:
+        tag, rep = item.split("=", 1)
+        data[tag] = read(rep)
+        data[tag]["report"] = os.path.basename(rep)
+    with open(args.out, "w") as fh:
+        json.dump(data, fh, indent=1)
+    if args.md:
+        lines = ["| kernel tag | us | DRAM R+W (MB) | DRAM % peak | FP64 pipe % | warps active % | regs | top stalls |",
+                 "|---|---|---|---|---|---|---|---|"]
+        for tag, r in data.items():
+            st = ", ".join(f"{k} {v}%" for k, v in list(r["stall_pct"].items())[:4])
+            lines.append(f"| {tag} | {r.get('duration_us', 0):.1f} | {r['dram_bytes_per_launch'] / 1e6:.1f} | "
+                         f"{r.get('dram_pct_peak', 0):.1f} | {r.get('fp64_pipe_pct', 0):.1f} | "
+                         f"{r.get('warps_active_pct', 0):.1f} | {r.get('registers', 0):.0f} | {st} |")
+        open(args.md, "w").write("\n".join(lines) + "\n")
+    print(json.dumps(data, indent=1)[:3000])
+
+
+if __name__ == "__main__":
+    main()

@@ -51,6 +51,12 @@ def main():
         out[f"fp64_blocks_{blocks}"] = {"tflops": vals, "ms_last": ms.value,
                                         "sm_mhz_median": sorted(clocks)[len(clocks) // 2] if clocks else None}
     out["fp64_tflops_best"] = best
+    vals = []
+    for _ in range(3):
+        assert lib.probe_fp32_peak(sms * 8, 200000, ctypes.byref(ms), ctypes.byref(tf)) == 0
+        vals.append(tf.value)
+    out["fp32_tflops"] = vals
+    out["fp32_tflops_best"] = max(vals)
     out["sms"] = sms
 
     n = 1 << 30
