@@ -53,7 +53,7 @@ def parse(argv=None):
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--cases", default="C1,C3,C4,C4f32", help="extra per-config kernel timings (N=1 only)")
+    ap.add_argument("--cases", default="C1,C3,C4,C4f32,C5", help="extra per-config kernel timings (N=1 only)")
     ap.add_argument("--no-cases", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -193,18 +193,25 @@ class _Null:
 
 
 def sample_parity(desc, geo_rows, cof_rows, A_dev, b_dev, count=8192, seed=0):
-    """Max relative Frobenius error of GPU outputs vs the oracle on `count` sampled elements."""
-    from oracle import numpy_oracle as O
+    """Max relative Frobenius error of GPU outputs vs the oracle on `count` sampled elements.
 
-    n = geo_rows.shape[0]
-    idx = np.unique(np.random.default_rng(seed).integers(0, n, size=min(count, n)))
+    geo_rows / cof_rows: (n, DS) numpy arrays, or flat CUDA tensors (device-generated inputs).
+    """
     import torch
 
+    from oracle import numpy_oracle as O
+
+    n = A_dev.shape[0]
+    idx = np.unique(np.random.default_rng(seed).integers(0, n, size=min(count, n)))
     it = torch.from_numpy(idx).to(A_dev.device)
+    if isinstance(geo_rows, torch.Tensor):
+        g = geo_rows.view(n, -1).index_select(0, it).double().cpu().numpy()
+        c = cof_rows.view(n, -1).index_select(0, it).double().cpu().numpy()
+    else:
+        g, c = geo_rows[idx], cof_rows[idx]
     A = A_dev.index_select(0, it).double().cpu().numpy()
     b = b_dev.index_select(0, it).double().cpu().numpy()
-    Ao, bo = O.integrate(desc.variant.value, desc.geometry_path.value, desc.problem.value, desc.element.value,
-                         geo_rows[idx], cof_rows[idx])
+    Ao, bo = O.integrate(desc.variant.value, desc.geometry_path.value, desc.problem.value, desc.element.value, g, c)
     return float(max(O.rel_frobenius(A, Ao).max(), O.rel_frobenius(b, bo).max())), int(idx.size)
 
 
@@ -219,11 +226,11 @@ def measure_case(key, steps, warmup, variant="qss"):
     cfg = mesh.bench_configs()[key.replace("f32", "")]
     et, pb = cfg.spec.element_type, cfg.problem
     desc = KernelDescriptor(Variant(variant), natural_path(et), pb, et)
-    geo_rows, cof_rows = mesh.config_rows(cfg)
-    n = geo_rows.shape[0]
+    n = cfg.spec.n_elements
     dt = torch.float32 if fp32 else torch.float64
-    geo = torch.from_numpy(geo_rows.reshape(-1)).to("cuda", dtype=dt)
-    cof = torch.from_numpy(cof_rows.reshape(-1)).to("cuda", dtype=dt)
+    geo64, cof64 = mesh.device_config(cfg)      # generated in HBM, bit-identical to the host mesh
+    geo, cof = (geo64.float(), cof64.float()) if fp32 else (geo64, cof64)
+    geo_rows, cof_rows = geo64, cof64
     rb = 4 if fp32 else 8
     per_set = n * (et.geometry_size + pb.coefficient_size(et) + et.n_shape * (et.n_shape + 1)) * rb
     sets = 1 if per_set > 3 * L2_BYTES else 3  # rotate buffer sets when one set is near L2 size
@@ -247,7 +254,71 @@ def measure_case(key, steps, warmup, variant="qss"):
         "parity": {"max_rel_frobenius": err, "elements_checked": cnt, "tolerance": tol, "pass": err <= tol,
                    "against": "numpy oracle (bitwise-pinned restatement of the reference)"},
     }
-    del launchers, geo, cof
+    del launchers, geo, cof, geo64, cof64, geo_rows, cof_rows
+    torch.cuda.empty_cache()
+    return rec
+
+
+def c5_parts(world: int, rank: int):
+    """(cfg, desc, first, n) of this rank's contiguous shards of the two C5 batches."""
+    from paper_1504_01023_b200 import KernelDescriptor, mesh, natural_path
+    from paper_1504_01023_b200.distributed import shard_bounds
+    from paper_1504_01023_b200.problems import Variant
+
+    parts = []
+    for key in ("C5T", "C5P"):
+        cfg = mesh.bench_configs()[key]
+        et = cfg.spec.element_type
+        lo, hi = shard_bounds(cfg.spec.n_elements, world, rank)
+        parts.append((cfg, KernelDescriptor(Variant.QSS, natural_path(et), cfg.problem, et), lo, hi - lo))
+    return parts
+
+
+def measure_c5(steps, warmup, world=1, rank=0, sampler=None):
+    """C5: 64M-element mixed CDR mesh = one tet batch + one prism batch, range-sharded.
+
+    A step integrates this rank's shard of both batches (two launches, same
+    stream).  Inputs are generated in HBM by the device mesh generator.
+    """
+    import torch
+
+    from paper_1504_01023_b200 import mesh
+    from paper_1504_01023_b200.kernels.counts import algorithmic_bytes, algorithmic_flops
+    from paper_1504_01023_b200.measure import flop_peak, hbm_peak
+
+    launchers, parts = [], c5_parts(world, rank)
+    for cfg, desc, lo, n in parts:
+        geo, cof = mesh.device_config(cfg, lo, n)
+        launchers.append((Launcher(desc, geo, cof, base_index=lo), desc, geo, cof))
+
+    def step():
+        for L, *_ in launchers:
+            L()
+
+    per, total_ms = time_launches([step], steps, warmup, sampler)
+    for L, *_ in launchers:
+        if L.error_key() != 0xFFFFFFFFFFFFFFFF:
+            raise RuntimeError(f"C5: unexpected geometry error key {L.error_key():#x}")
+    ms = total_ms / steps
+    n_local = sum(n for *_, n in parts)
+    hbm, _ = hbm_peak()
+    fp, _ = flop_peak(8)
+    by = sum(algorithmic_bytes(d.element, d.problem) * n for _, d, _, n in parts)
+    fl = sum(algorithmic_flops(d.element, d.problem) * n for _, d, _, n in parts)
+    t_roof = max(by / (hbm * 1e9), fl / (fp * 1e12))
+    serial = sum(max(algorithmic_bytes(d.element, d.problem) * n / (hbm * 1e9),
+                     algorithmic_flops(d.element, d.problem) * n / (fp * 1e12)) for _, d, _, n in parts)
+    parity = {}
+    for (L, desc, geo, cof), (cfg, *_) in zip(launchers, parts):
+        err, cnt = sample_parity(desc, geo, cof, L.A, L.b, count=4096)
+        parity[cfg.key] = {"max_rel_frobenius": err, "elements_checked": cnt, "pass": err <= 1e-12}
+    rec = {"workload": "C5: 64,156,250-element mixed CDR mesh (175^3x6 tets + 4000^2x2 jittered prisms)",
+           "elements_this_rank": n_local, "ms_per_step": ms, "value_this_rank": n_local / (ms / 1e3),
+           "roofline": {"bound": "concurrent max(sum bytes/HBM, sum flops/FP64)", "roof_ms": t_roof * 1e3,
+                        "frac": t_roof / (ms / 1e3), "serialized_by_type_roof_ms": serial * 1e3,
+                        "frac_of_serialized": serial / (ms / 1e3)},
+           "parity": parity}
+    del launchers
     torch.cuda.empty_cache()
     return rec
 
@@ -399,7 +470,8 @@ def run_ours(args) -> int:
         cases = {}
         for key in [c for c in args.cases.split(",") if c]:
             try:
-                cases[key] = measure_case(key, args.steps, args.warmup)
+                cases[key] = measure_c5(args.steps, args.warmup) if key == "C5" else \
+                    measure_case(key, args.steps, args.warmup)
             except Exception as exc:  # keep the headline line even if a case fails
                 cases[key] = {"error": f"{type(exc).__name__}: {exc}"}
         out["cases"] = cases
@@ -412,10 +484,51 @@ def run_ours(args) -> int:
     return 0
 
 
+def run_c5(args) -> int:
+    """--config C5: the 64M mixed mesh, strong scaling (each rank generates and integrates its shard)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1504_01023_b200.distributed import env_rank
+    from paper_1504_01023_b200.measure import ClockSampler, clocks_rejected
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier()
+    sampler = ClockSampler(local, period=0.0005)
+    rec = measure_c5(args.steps, args.warmup, world, rank, sampler)
+    t = torch.tensor([rec["ms_per_step"]], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    total = 64_156_250
+    if rank == 0:
+        clocks = sampler.summary()
+        line = {"metric": METRIC, "value": total / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic: reference meshes generated in HBM (device PCG64, bit-identical to numpy)",
+                "config": {"workload": rec["workload"], "elements_total": total,
+                           "parallelism": f"element-range shards x{world} of both batches, no collective"},
+                "clocks": clocks, "e2e": None, "gpu_launches": 2 * args.steps,
+                "roofline": rec["roofline"], "parity_rank0": rec["parity"]}
+        if clocks_rejected(clocks):
+            line["clocks_warning"] = clocks_rejected(clocks)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main(argv=None) -> int:
     args = parse(argv)
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "C5":
+        return run_c5(args)
     return run_ours(args)
 
 

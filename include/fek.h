@@ -136,6 +136,26 @@ size_t fek_checksum_scratch_bytes(void);
 int fek_checksum(const fek_batch_desc *d, void *partials, double *out_f64,
                  unsigned long long *out_u64, void *cuda_stream);
 
+/* ---- device-side synthetic inputs ----------------
+ * Replace the host generator pkg/src/feklab/mesh.py:49-109 for the benchmark
+ * configurations: outputs are bit-identical to the host (numpy) version for
+ * any element / draw range, so each GPU of a sharded run can generate exactly
+ * its slice of the global mesh.
+ *
+ * `stream` = numpy PCG64 state as 4 words {state_hi, state_lo, inc_hi, inc_lo}
+ * (np.random.PCG64(seed).state).  fek_pcg64_uniform writes draws
+ * [first, first + count) of Generator.uniform(low, high). */
+int fek_pcg64_uniform(const unsigned long long *stream, int64_t first, int64_t count, double low, double high,
+                      double *out, void *cuda_stream);
+
+/* Element-major geometry rows of elements [first, first + n) of the
+ * reference unit-cube mesh (Kuhn tets nx*ny*nz*6, or extruded prisms
+ * nx*ny*2); prisms optionally get the top-face jitter of
+ * mesh.jitter_top_faces (jitter_stream may be NULL). */
+int fek_mesh_geometry(int32_t element, int64_t nx, int64_t ny, int64_t nz, int64_t first, int64_t n,
+                      const unsigned long long *jitter_stream, double jitter_amplitude, double *out,
+                      void *cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

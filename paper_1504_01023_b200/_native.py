@@ -72,6 +72,11 @@ SIGNATURES = {
     "fek_error_detail": (ctypes.c_int, [_DP, ctypes.c_int64, ctypes.c_int32, _P, _P]),
     "fek_checksum_scratch_bytes": (ctypes.c_size_t, []),
     "fek_checksum": (ctypes.c_int, [_DP, _P, _P, _P, _P]),
+    "fek_pcg64_uniform": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int64, ctypes.c_int64,
+                                         ctypes.c_double, ctypes.c_double, _P, _P]),
+    "fek_mesh_geometry": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                         ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_ulonglong),
+                                         ctypes.c_double, _P, _P]),
 }
 
 _lib = None

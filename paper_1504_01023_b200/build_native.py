@@ -46,7 +46,8 @@ def _nvcc() -> str:
 
 
 def _sources() -> list[str]:
-    return [os.path.join(CSRC, "fek_abi.cu")] + sorted(glob.glob(os.path.join(CSRC, "cases", "*.cu")))
+    return [os.path.join(CSRC, "fek_abi.cu"), os.path.join(CSRC, "fek_mesh.cu")] + sorted(
+        glob.glob(os.path.join(CSRC, "cases", "*.cu")))
 
 
 def _headers() -> list[str]:

@@ -164,7 +164,7 @@ def bench_configs() -> dict[str, BenchConfig]:
                           "Convection-diffusion-reaction on 16M non-affine linear prisms"),
         "C5T": BenchConfig("C5T", MeshSpec(175, 175, 175, T), ProblemClass.CONV_DIFF, 0, None,
                            "C5 tet part: 32.2M tets, convection-diffusion-reaction"),
-        "C5P": BenchConfig("C5P", MeshSpec(4000, 4000, 1, P), ProblemClass.CONV_DIFF, 1, 1,
+        "C5P": BenchConfig("C5P", MeshSpec(4000, 4000, 1, P), ProblemClass.CONV_DIFF, 1, 2,
                            "C5 prism part: 32M non-affine prisms, convection-diffusion-reaction"),
     }
 
@@ -174,3 +174,64 @@ def config_rows(cfg: BenchConfig) -> tuple[np.ndarray, np.ndarray]:
     if cfg.jitter_seed is not None:
         geo = jitter_top_faces(geo, cfg.spec, cfg.jitter_seed)
     return geo, coefficient_rows(cfg.spec.n_elements, cfg.problem, cfg.spec.element_type, cfg.coeff_seed)
+
+
+# ---------------------------------------------------------------------------
+# device-side generation (libfek fek_mesh_geometry / fek_pcg64_uniform)
+# ---------------------------------------------------------------------------
+
+def pcg64_words(seed: int):
+    """numpy PCG64(seed) state as the 4-word array fek_pcg64_uniform takes."""
+    import ctypes
+
+    st = np.random.PCG64(seed).state["state"]
+    mask = (1 << 64) - 1
+    words = [(st["state"] >> 64) & mask, st["state"] & mask, (st["inc"] >> 64) & mask, st["inc"] & mask]
+    return (ctypes.c_ulonglong * 4)(*words)
+
+
+def device_geometry(spec: MeshSpec, first: int = 0, n: int | None = None, jitter_seed: int | None = None,
+                    amplitude: float = 0.15, device=None):
+    """Geometry rows of elements [first, first+n) generated in HBM (flat float64 tensor).
+
+    Bit-identical to ``geometry_rows(spec)[first:first+n]`` (plus
+    ``jitter_top_faces(..., jitter_seed)``); no host work.
+    """
+    import torch
+
+    from . import _native
+
+    n = spec.n_elements - first if n is None else n
+    out = torch.empty(n * spec.element_type.geometry_size, dtype=torch.float64, device=device or "cuda")
+    lib = _native.load()
+    js = pcg64_words(jitter_seed) if jitter_seed is not None else None
+    code = _native.ELEMENT[spec.element_type.value]
+    with torch.cuda.device(out.device):
+        _native.check(lib.fek_mesh_geometry(code, spec.nx, spec.ny, spec.nz, first, n, js, amplitude,
+                                            out.data_ptr(), torch.cuda.current_stream().cuda_stream),
+                      "fek_mesh_geometry")
+    return out
+
+
+def device_coefficients(problem: ProblemClass, element_type: ElementType, seed: int, first: int, n: int,
+                        device=None):
+    """Coefficient rows [first, first+n) of ``coefficient_rows(..., seed)`` generated in HBM."""
+    import torch
+
+    from . import _native
+
+    ds = problem.coefficient_size(element_type)
+    out = torch.empty(n * ds, dtype=torch.float64, device=device or "cuda")
+    lib = _native.load()
+    with torch.cuda.device(out.device):
+        _native.check(lib.fek_pcg64_uniform(pcg64_words(seed), first * ds, n * ds, -1.0, 1.0, out.data_ptr(),
+                                            torch.cuda.current_stream().cuda_stream), "fek_pcg64_uniform")
+    return out
+
+
+def device_config(cfg: BenchConfig, first: int = 0, n: int | None = None, device=None):
+    """(geometry, coefficients) flat float64 CUDA tensors of elements [first, first+n) of a config."""
+    n = cfg.spec.n_elements - first if n is None else n
+    geo = device_geometry(cfg.spec, first, n, cfg.jitter_seed, device=device)
+    cof = device_coefficients(cfg.problem, cfg.spec.element_type, cfg.coeff_seed, first, n, device=device)
+    return geo, cof
