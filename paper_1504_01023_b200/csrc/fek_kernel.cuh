@@ -58,10 +58,14 @@ struct Traits {
   // the staged tile instead of pinning 18 reals in registers
   static constexpr bool LAZY_X = (GEO == GEO_GENERIC) && (ET == PRISM || VAR != QSS);
   // stages / resident CTAs: memory-bound tets keep >= 64 KB of loads in
-  // flight per SM; the FP64-bound prism CDR kernel needs its shared memory
-  // for two resident CTAs (8 warps) more than for a second stage
-  static constexpr int STAGES = (ET == TET && PB == POISSON) ? 3 : ((LAZY_X && PB == CONV_DIFF) ? 1 : 2);
-  static constexpr int MIN_BLOCKS = (ET == TET && PB == POISSON) ? 3 : 2;
+  // flight per SM; the prism kernels spend shared memory on resident warps
+  // (latency hiding for the FP64 pipe) rather than on a second stage
+  // prism Poisson: 3 resident CTAs (12 warps, <= 170 registers, one stage)
+  // beat 2 CTAs with two stages by 4% (C3 0.428 vs 0.445 ms, same-session A/B)
+  static constexpr bool PRISM_P = (ET == PRISM && PB == POISSON);
+  static constexpr int STAGES =
+      (PRISM_P || (LAZY_X && PB == CONV_DIFF)) ? 1 : ((ET == TET && PB == POISSON) ? 3 : 2);
+  static constexpr int MIN_BLOCKS = (PRISM_P || (ET == TET && PB == POISSON)) ? 3 : 2;
   static constexpr unsigned GEO_TILE_BYTES = TILE * DSG * sizeof(R);
   static constexpr unsigned COEF_TILE_BYTES = TILE * DSC * sizeof(R);
   static constexpr unsigned OUT_A_BYTES = TILE * NA * sizeof(R);
