@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import paper_1504_01023_b200 as fek
-from conftest import golden
+from conftest import GOLDEN, golden
 from oracle import numpy_oracle as O
 from paper_1504_01023_b200 import (BatchLayout, CoefficientSet, DeviceBatch, ElementBatch, ElementGeometry,
                                    ElementType, GeometryPath, KernelDescriptor, LayoutKind, ProblemClass,
@@ -144,8 +144,7 @@ def _error_cases():
 def test_geometry_errors_match_reference():
     import torch
 
-    msgs = dict(line.split("\t", 1) for line in open(golden.__globals__["GOLDEN"] + "/error_messages.tsv")
-                .read().strip().split("\n"))
+    msgs = dict(line.split("\t", 1) for line in open(GOLDEN + "/error_messages.tsv").read().strip().split("\n"))
     checked = 0
     for z, name, et, pb, geo, cof in _error_cases():
         batch = ElementBatch.from_arrays(et, pb, geo, cof)
