@@ -480,13 +480,13 @@ __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef,
   using S = Shape<ET>;
   constexpr int NS = S::NS, NQ = S::NQ, DSG = 3 * S::NV;
   constexpr bool SYM = (PB == POISSON);
-  kind = 0;
-  kind_point = -1;
+  // failing points as bitmasks (branch-free); the reported point is the
+  // SMALLEST failing q, as in the reference (q = 0, 1, ... checked in order;
+  // prism points are visited zeta-major here)
+  unsigned fail_mask = 0, degen_mask = 0;
   auto note = [&](int k, int q) {
-    if (k && !kind) {
-      kind = k;
-      kind_point = q;
-    }
+    fail_mask |= static_cast<unsigned>(k != 0) << q;
+    degen_mask |= static_cast<unsigned>(k == KIND_DEGENERATE) << q;
   };
 #pragma unroll
   for (int i = 0; i < NS * NS; ++i) A[i] = R(0);
@@ -605,6 +605,12 @@ __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef,
     for (int r = 0; r < NS; ++r)
 #pragma unroll
       for (int s = 0; s < r; ++s) A[NS * r + s] = A[NS * s + r];
+  }
+  kind = 0;
+  kind_point = -1;
+  if (fail_mask) {
+    kind_point = __ffs(fail_mask) - 1;
+    kind = ((degen_mask >> kind_point) & 1u) ? KIND_DEGENERATE : KIND_INVERTED;
   }
 }
 

@@ -175,6 +175,10 @@ def error_cases():
     degenerate_prism[3:] = degenerate_prism[:3]
     cases["prism_degenerate_2"] = (prism_batch(6, {2: degenerate_prism}), PRISM, CONVDIFF)
     cases["prism_partial_5_full_7"] = (prism_batch(12, {5: partly, 7: -good}), PRISM, CONVDIFF)
+    # fails at q = 1..5 but not at q = 0: the reported point must be the
+    # smallest failing q (1), not the first one a zeta-major traversal meets (2)
+    min_q = np.array([[1.0735260056398386, 0.12576261533222466, -0.8115836684702022], [1.477080626165721, -1.160412031527824, -0.07387428460248158], [-0.12848346302867486, 0.18727422292154416, 0.00080667169439685], [-1.1216759257033364, 0.411796613002633, -0.23779211946897516], [0.7747694645679373, 0.767314309052276, 1.2606507785965007], [-0.7160999048204778, 0.18610641169245237, 2.4502436484894625]])
+    cases["prism_min_q_3"] = (prism_batch(8, {3: min_q}), PRISM, CONVDIFF)
     # block rule: element 8200 fails at q=0 (block 1), element 100 only at a
     # later q (block 0).  Geometry is a formula (block_rule_rows) so the
     # fixture does not have to store 8300 elements.
