@@ -62,6 +62,11 @@ def parse(argv=None):
     return ap.parse_args(argv)
 
 
+def launched_by_torchrun() -> bool:
+    """Under torchrun (any N, including 1) the NCCL process group is initialised."""
+    return "WORLD_SIZE" in os.environ and "MASTER_ADDR" in os.environ
+
+
 def _config_record(cfg, n_per_rank, world, desc, extra=None):
     rec = {
         "workload": f"{cfg.key}: {cfg.text}",
@@ -350,7 +355,8 @@ def run_ours(args) -> int:
         print(json.dumps({"metric": METRIC, "error": "no CUDA device"}))
         return 1
     torch.cuda.set_device(local)
-    if world > 1:
+    distributed = launched_by_torchrun()
+    if distributed:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     cfg = mesh.bench_configs()[args.config]
@@ -364,7 +370,7 @@ def run_ours(args) -> int:
     launcher = Launcher(desc, dev_batch.geometry_data, dev_batch.coefficient_data, base_index=rank * n)
 
     # ---- device-resident timing (the `value`) ----
-    if world > 1:
+    if distributed:
         dist.barrier()
     torch.cuda.synchronize()
     sampler = ClockSampler(local, period=0.0005)
@@ -375,7 +381,7 @@ def run_ours(args) -> int:
     step_ms = total_ms / args.steps
     launch_ms = float(np.mean(per))
     t = torch.tensor([step_ms, launch_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
+    if distributed:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     step_ms, launch_ms = t.tolist()
     value = world * n / (step_ms / 1e3)
@@ -401,7 +407,7 @@ def run_ours(args) -> int:
         res = integrate_batch(desc, host_batch, base_index=rank * n)
         res = integrate_batch(desc, host_batch, base_index=rank * n)
         torch.cuda.synchronize()
-        if world > 1:
+        if distributed:
             dist.barrier()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
@@ -411,7 +417,7 @@ def run_ours(args) -> int:
         torch.cuda.synchronize()
         ms = s.elapsed_time(e) / e2e_steps
         tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        if world > 1:
+        if distributed:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
         h2d = host_batch.geometry_data.nbytes + host_batch.coefficient_data.nbytes
@@ -476,9 +482,23 @@ def run_ours(args) -> int:
                 cases[key] = {"error": f"{type(exc).__name__}: {exc}"}
         out["cases"] = cases
 
+    if distributed:
+        # verification after timing: every rank's error word must be clear;
+        # bit-pattern sums of all shards reduced over NCCL (reported, not timed)
+        from paper_1504_01023_b200.distributed import allreduce_error_key, allreduce_sums, device_checksum
+        from paper_1504_01023_b200.kernels.batched import BatchResult, _traffic
+
+        key_all = allreduce_error_key(launcher.error_key())
+        res = BatchResult(desc, n, launcher.A, launcher.b, _traffic(desc, n))
+        f, u = allreduce_sums(*device_checksum(res, base_index=rank * n))
+        if rank == 0:
+            out["verification"] = {"error_key_all_ranks": "none" if key_all == 0xFFFFFFFFFFFFFFFF else hex(key_all),
+                                   "sum_A": float(f[0]), "sum_abs_A": float(f[2]),
+                                   "bitsum_A": int(u[0].item()) & 0xFFFFFFFFFFFFFFFF,
+                                   "collectives": "NCCL all_reduce(MIN error key, SUM checksums) after timing"}
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if distributed:
         dist.barrier()
         dist.destroy_process_group()
     return 0
@@ -494,13 +514,14 @@ def run_c5(args) -> int:
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
-    if world > 1:
+    distributed = launched_by_torchrun()
+    if distributed:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist.barrier()
     sampler = ClockSampler(local, period=0.0005)
     rec = measure_c5(args.steps, args.warmup, world, rank, sampler)
     t = torch.tensor([rec["ms_per_step"]], dtype=torch.float64, device="cuda")
-    if world > 1:
+    if distributed:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     total = 64_156_250
@@ -517,7 +538,7 @@ def run_c5(args) -> int:
         if clocks_rejected(clocks):
             line["clocks_warning"] = clocks_rejected(clocks)
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         dist.barrier()
         dist.destroy_process_group()
     return 0
