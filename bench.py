@@ -53,7 +53,8 @@ def parse(argv=None):
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--cases", default="C1,C3,C4,C4f32,C5", help="extra per-config kernel timings (N=1 only)")
+    ap.add_argument("--cases", default="C1,C3,C4,C4f32,C5,C2packed",
+                    help="extra per-config kernel timings (N=1 only)")
     ap.add_argument("--no-cases", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -135,7 +136,7 @@ def run_reference(args) -> int:
 class Launcher:
     """Prepared fek_integrate call on device tensors (no Python work per launch but ctypes)."""
 
-    def __init__(self, desc, geo, cof, base_index=0, layout=None):
+    def __init__(self, desc, geo, cof, base_index=0, layout=None, packed_layout=None):
         import torch
 
         from paper_1504_01023_b200 import ELEMENT_MAJOR, _native
@@ -146,13 +147,23 @@ class Launcher:
         ns = et.n_shape
         n = geo.numel() // et.geometry_size
         self.n = n
-        self.A = torch.empty((n, ns, ns), dtype=geo.dtype, device=geo.device)
-        self.b = torch.empty((n, ns), dtype=geo.dtype, device=geo.device)
         self.err = torch.full((1,), -1, dtype=torch.int64, device=geo.device)
         self.keep = (geo, cof)
         code = _native.DTYPE["float64" if geo.dtype == torch.float64 else "float32"]
+        if packed_layout is None:
+            self.A = torch.empty((n, ns, ns), dtype=geo.dtype, device=geo.device)
+            self.b = torch.empty((n, ns), dtype=geo.dtype, device=geo.device)
+            ptrs = (self.A.data_ptr(), self.b.data_ptr())
+        else:  # kernel writes flat_output() rows [A | b] directly
+            from paper_1504_01023_b200 import flat_length
+
+            self.flat = torch.empty(flat_length(n, ns * ns + ns, packed_layout), dtype=geo.dtype, device=geo.device)
+            rows = self.flat.view(-1, ns * ns + ns)[:n] if packed_layout.lane_width == 1 else None
+            self.A = rows[:, : ns * ns].unflatten(1, (ns, ns)) if rows is not None else None
+            self.b = rows[:, ns * ns:] if rows is not None else None
+            ptrs = (self.flat.data_ptr(), 0)
         self.dd = _desc_struct(desc, layout or ELEMENT_MAJOR, n, base_index, code, geo.data_ptr(), cof.data_ptr(),
-                               self.A.data_ptr(), self.b.data_ptr(), self.err.data_ptr())
+                               ptrs[0], ptrs[1], self.err.data_ptr(), out_layout=packed_layout)
         self.ref = ctypes.byref(self.dd)
         self.stream = torch.cuda.current_stream().cuda_stream
 
@@ -228,7 +239,8 @@ def measure_case(key, steps, warmup, variant="qss"):
     from paper_1504_01023_b200.problems import Variant
 
     fp32 = key.endswith("f32")
-    cfg = mesh.bench_configs()[key.replace("f32", "")]
+    packed = key.endswith("packed")
+    cfg = mesh.bench_configs()[key.replace("f32", "").replace("packed", "")]
     et, pb = cfg.spec.element_type, cfg.problem
     desc = KernelDescriptor(Variant(variant), natural_path(et), pb, et)
     n = cfg.spec.n_elements
@@ -239,9 +251,12 @@ def measure_case(key, steps, warmup, variant="qss"):
     rb = 4 if fp32 else 8
     per_set = n * (et.geometry_size + pb.coefficient_size(et) + et.n_shape * (et.n_shape + 1)) * rb
     sets = 1 if per_set > 3 * L2_BYTES else 3  # rotate buffer sets when one set is near L2 size
-    launchers = [Launcher(desc, geo, cof)]
+    from paper_1504_01023_b200 import ELEMENT_MAJOR
+
+    pk = ELEMENT_MAJOR if packed else None
+    launchers = [Launcher(desc, geo, cof, packed_layout=pk)]
     for _ in range(sets - 1):
-        launchers.append(Launcher(desc, geo.clone(), cof.clone()))
+        launchers.append(Launcher(desc, geo.clone(), cof.clone(), packed_layout=pk))
     per, _ = time_launches(launchers, steps, warmup)
     for L in launchers:
         if L.error_key() != 0xFFFFFFFFFFFFFFFF:
@@ -250,7 +265,8 @@ def measure_case(key, steps, warmup, variant="qss"):
     err, cnt = sample_parity(desc, geo_rows, cof_rows, launchers[0].A, launchers[0].b)
     tol = 1e-3 if fp32 else 1e-12
     rec = {
-        "workload": cfg.text + (" (fp32)" if fp32 else " (fp64)"),
+        "workload": cfg.text + (" (fp32)" if fp32 else " (fp64)") +
+                    (", kernel-packed flat_output rows" if packed else ""),
         "elements": n, "descriptor": desc.short_name(), "dtype": "f32" if fp32 else "f64",
         "value": n / (ms / 1e3), "unit": UNIT, "ms_per_launch": ms, "ms_min": float(np.min(per)),
         "buffer_sets": sets,

@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define FEK_ABI_VERSION 1
+#define FEK_ABI_VERSION 2
 
 /* enums mirror the Python ones (refelem.py:29, problems.py:26-49) */
 enum fek_element { FEK_TETRAHEDRON = 0, FEK_PRISM = 1 };
@@ -56,6 +56,10 @@ enum fek_variant { FEK_QSS = 0, FEK_SQS = 1, FEK_SSQ = 2 };
 enum fek_geometry_path { FEK_GEO_LINEAR = 0, FEK_GEO_GENERIC = 1 };
 enum fek_dtype { FEK_F64 = 0, FEK_F32 = 1 };
 enum fek_layout_kind { FEK_ELEMENT_MAJOR = 0, FEK_LANE_INTERLEAVED = 1 };
+/* output format: split arrays (BatchResult.stiffness / .load, batched.py:566-567)
+ * or packed rows [A row-major | b] per element in the output layout
+ * (BatchResult.flat_output, batched.py:99-106, layout.py:72-82) */
+enum fek_out_format { FEK_OUT_SPLIT = 0, FEK_OUT_PACKED = 1 };
 
 /* status codes */
 enum fek_status {
@@ -81,14 +85,18 @@ typedef struct fek_batch_desc {
   int32_t dtype;          /* enum fek_dtype: real type of all four arrays        */
   int32_t layout;         /* enum fek_layout_kind of geometry/coefficients       */
   int32_t lane_width;     /* W in {1,4,8,16,32,64}; 1 for element-major         */
-  int32_t reserved;
+  int32_t out_format;     /* enum fek_out_format                                 */
   int64_t n_elements;     /* elements covered by this call                       */
   int64_t base_index;     /* absolute index of element 0 (errors, sharding)      */
   const void *geometry;   /* flat geometry_data  (3*nv reals per element)        */
   const void *coefficients; /* flat coefficient_data (nq or 20 reals)            */
-  void *stiffness;        /* (n, ns, ns) reals                                   */
-  void *load;             /* (n, ns) reals                                       */
+  void *stiffness;        /* SPLIT: (n, ns, ns) reals.  PACKED: the flat packed
+                             array, flat_length(n, ns*ns + ns, out layout) reals,
+                             lane-interleaved pad lanes written as NaN           */
+  void *load;             /* SPLIT: (n, ns) reals.  PACKED: unused (NULL)         */
   unsigned long long *error_key; /* device word (fek_integrate), init FEK_NO_ERROR */
+  int32_t out_lane_width; /* PACKED: output lane width W (1 = element-major rows)  */
+  int32_t reserved;
 } fek_batch_desc;
 
 int fek_abi_version(void);

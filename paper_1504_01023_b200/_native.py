@@ -19,7 +19,7 @@ if os.environ.get("FEK_LIB_OVERRIDE"):  # kernel-tuning experiments only
     LIB_PATH = os.path.abspath(os.environ["FEK_LIB_OVERRIDE"])
 HEADER_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "fek.h")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 NO_ERROR = 0xFFFFFFFFFFFFFFFF
 
 OK, ERR_ARGUMENT, ERR_ALIGNMENT, ERR_CUDA, ERR_WORKSPACE, ERR_GEOMETRY = range(6)
@@ -32,6 +32,7 @@ VARIANT = {"qss": 0, "sqs": 1, "ssq": 2}
 GEO_PATH = {"linear": 0, "generic": 1}
 DTYPE = {"float64": 0, "float32": 1}
 LAYOUT = {"major": 0, "interleaved": 1}
+OUT_SPLIT, OUT_PACKED = 0, 1
 
 
 class BatchDesc(ctypes.Structure):
@@ -43,7 +44,7 @@ class BatchDesc(ctypes.Structure):
         ("dtype", ctypes.c_int32),
         ("layout", ctypes.c_int32),
         ("lane_width", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("out_format", ctypes.c_int32),
         ("n_elements", ctypes.c_int64),
         ("base_index", ctypes.c_int64),
         ("geometry", ctypes.c_void_p),
@@ -51,6 +52,8 @@ class BatchDesc(ctypes.Structure):
         ("stiffness", ctypes.c_void_p),
         ("load", ctypes.c_void_p),
         ("error_key", ctypes.c_void_p),
+        ("out_lane_width", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 

@@ -97,9 +97,16 @@ int validate(const fek_batch_desc *d, bool need_pointers) {
     return FEK_ERR_ARGUMENT;
   }
   if (d->n_elements < 0 || d->base_index < 0) return FEK_ERR_ARGUMENT;
+  const bool packed = d->out_format == FEK_OUT_PACKED;
+  if (!packed && d->out_format != FEK_OUT_SPLIT) return FEK_ERR_ARGUMENT;
+  if (packed) {
+    const int w = d->out_lane_width;
+    if (!(w == 1 || w == 4 || w == 8 || w == 16 || w == 32 || w == 64)) return FEK_ERR_ARGUMENT;
+  }
   if (need_pointers && d->n_elements > 0) {
-    if (!d->geometry || !d->coefficients || !d->stiffness || !d->load) return FEK_ERR_ARGUMENT;
-    if (!aligned16(d->geometry) || !aligned16(d->coefficients) || !aligned16(d->stiffness) || !aligned16(d->load))
+    if (!d->geometry || !d->coefficients || !d->stiffness || (!packed && !d->load)) return FEK_ERR_ARGUMENT;
+    if (!aligned16(d->geometry) || !aligned16(d->coefficients) || !aligned16(d->stiffness) ||
+        (!packed && !aligned16(d->load)))
       return FEK_ERR_ALIGNMENT;
   }
   return FEK_OK;
@@ -129,6 +136,8 @@ int launch(const fek_batch_desc *d, cudaStream_t stream, int *grid_out, int *blo
   p.n = d->n_elements;
   p.base = d->base_index;
   p.lane_width = d->layout == FEK_ELEMENT_MAJOR ? 1 : d->lane_width;
+  p.out_packed = d->out_format == FEK_OUT_PACKED;
+  p.out_width = p.out_packed ? d->out_lane_width : 1;
   ke.fn<<<grid, ke.threads, ke.smem, stream>>>(p);
   FEK_CUDA(cudaGetLastError());
   return FEK_OK;
@@ -277,7 +286,7 @@ size_t fek_checksum_scratch_bytes(void) { return static_cast<size_t>(kSumBlocks)
 int fek_checksum(const fek_batch_desc *d, void *partials, double *out_f64, unsigned long long *out_u64,
                  void *cuda_stream) {
   if (int rc = validate(d, false)) return rc;
-  if (!partials || !out_f64 || !out_u64) return FEK_ERR_ARGUMENT;
+  if (!partials || !out_f64 || !out_u64 || d->out_format != FEK_OUT_SPLIT) return FEK_ERR_ARGUMENT;
   if (d->n_elements > 0 && (!d->stiffness || !d->load)) return FEK_ERR_ARGUMENT;
   cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
   double *pf = static_cast<double *>(partials);
@@ -314,7 +323,7 @@ SlotPlan slot_plan(const fek_batch_desc *d, long long chunk) {
   SlotPlan p;
   p.geo = round256(chunk * geometry_size(d->element) * rb);
   p.coef = round256(chunk * coefficient_size(d->element, d->problem) * rb);
-  p.A = round256(chunk * ns * ns * rb);
+  p.A = round256(chunk * (ns * ns + ns) * rb);  // packed rows need ns*ns + ns per element
   p.b = round256(chunk * ns * rb);
   p.slot = p.geo + p.coef + p.A + p.b;
   return p;
@@ -342,7 +351,8 @@ int fek_integrate_host(const fek_batch_desc *d, void *device_workspace, size_t w
   *error_key_out = FEK_NO_ERROR;
   const long long n = d->n_elements;
   if (n == 0) return FEK_OK;
-  if (!d->geometry || !d->coefficients || !d->stiffness || !d->load) return FEK_ERR_ARGUMENT;
+  if (!d->geometry || !d->coefficients || !d->stiffness || (d->out_format == FEK_OUT_SPLIT && !d->load))
+    return FEK_ERR_ARGUMENT;
 
   char *ws = static_cast<char *>(device_workspace);
   unsigned long long *dkey = reinterpret_cast<unsigned long long *>(ws);
@@ -390,8 +400,14 @@ int fek_integrate_host(const fek_batch_desc *d, void *device_workspace, size_t w
     cd.error_key = dkey;
     rc = launch(&cd, st, nullptr, nullptr, nullptr, nullptr, true);
     if (rc) break;
-    e = cudaMemcpyAsync(hA + lo * ns * ns * rb, dA, cnt * ns * ns * rb, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(hb + lo * ns * rb, db, cnt * ns * rb, cudaMemcpyDeviceToHost, st);
+    if (d->out_format == FEK_OUT_PACKED) {
+      const int dso = ns * ns + ns;
+      e = cudaMemcpyAsync(hA + lo * dso * rb, dA, flat_len(cnt, dso, d->out_lane_width) * rb, cudaMemcpyDeviceToHost,
+                          st);
+    } else {
+      e = cudaMemcpyAsync(hA + lo * ns * ns * rb, dA, cnt * ns * ns * rb, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(hb + lo * ns * rb, db, cnt * ns * rb, cudaMemcpyDeviceToHost, st);
+    }
     if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync D2H");
   }
   for (int i = 0; i < n_streams; ++i) {

@@ -307,6 +307,21 @@ struct RowIO {
     }
   }
 
+  // lane-interleaved output tile (datum d of element l at (l/W)*W*DS + d*W + l%W)
+  __device__ __forceinline__ static void store_interleaved(uint32_t tile, int l, int w, const R (&in)[DS]) {
+    const uint32_t base = tile + static_cast<uint32_t>((l / w) * w * DS + (l % w)) * sizeof(R);
+    const uint32_t stride = static_cast<uint32_t>(w) * sizeof(R);
+#pragma unroll
+    for (int d = 0; d < DS; ++d) {
+      if constexpr (sizeof(R) == 8) {
+        sts64(base + d * stride, make_uint2(static_cast<uint32_t>(__double2loint(in[d])),
+                                            static_cast<uint32_t>(__double2hiint(in[d]))));
+      } else {
+        sts32(base + d * stride, __float_as_uint(in[d]));
+      }
+    }
+  }
+
   // element-major output tile
   __device__ __forceinline__ static void store_major(uint32_t tile, int l, const R (&in)[DS]) {
     const uint32_t row = tile + static_cast<uint32_t>(l) * BYTES;

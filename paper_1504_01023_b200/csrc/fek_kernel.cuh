@@ -41,6 +41,8 @@ struct LaunchParams {
   long long n;
   long long base;
   int lane_width;
+  int out_packed;  // FEK_OUT_PACKED: rows [A | b] into `stiffness` in the output layout
+  int out_width;   // output lane width (1 = element-major rows)
 };
 
 template <typename R_, int ET_, int PB_, int VAR_, int GEO_>
@@ -63,9 +65,11 @@ struct Traits {
   // prism Poisson: 3 resident CTAs (12 warps, <= 170 registers, one stage)
   // beat 2 CTAs with two stages by 4% (C3 0.428 vs 0.445 ms, same-session A/B)
   static constexpr bool PRISM_P = (ET == PRISM && PB == POISSON);
-  static constexpr int STAGES =
-      (PRISM_P || (LAZY_X && PB == CONV_DIFF)) ? 1 : ((ET == TET && PB == POISSON) ? 3 : 2);
-  static constexpr int MIN_BLOCKS = (PRISM_P || (ET == TET && PB == POISSON)) ? 3 : 2;
+  // fp32 prism CDR (168 registers, half the smem) fits 3 CTAs with 2 stages
+  static constexpr bool F32_PRISM_CD = (sizeof(R) == 4 && ET == PRISM && PB == CONV_DIFF);
+  static constexpr int STAGES = F32_PRISM_CD ? 2 :
+      ((PRISM_P || (LAZY_X && PB == CONV_DIFF)) ? 1 : ((ET == TET && PB == POISSON) ? 3 : 2));
+  static constexpr int MIN_BLOCKS = (F32_PRISM_CD || PRISM_P || (ET == TET && PB == POISSON)) ? 3 : 2;
   static constexpr unsigned GEO_TILE_BYTES = TILE * DSG * sizeof(R);
   static constexpr unsigned COEF_TILE_BYTES = TILE * DSC * sizeof(R);
   static constexpr unsigned OUT_A_BYTES = TILE * NA * sizeof(R);
@@ -194,6 +198,37 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
     if (kind) atomicMin(p.error_key, make_error_key(e_abs, kind_point, kind));
     if (tid == 0) bulk_wait_read<0>();
     __syncthreads();
+    if (p.out_packed) {
+      // packed rows [A row-major | b] (BatchResult.output_rows) laid out in
+      // the output layout; pad lanes of a partial interleaved block get NaN
+      // (pack_rows' default pad, layout.py:72-82)
+      constexpr int DSO = K::NA + K::NS;
+      const int w = p.out_width;
+      const int padded = ((count + w - 1) / w) * w;
+      if (tid < padded) {
+        R row[DSO];
+#pragma unroll
+        for (int k = 0; k < K::NA; ++k) row[k] = active ? A[k] : R(__longlong_as_double(0x7ff8000000000000ll));
+#pragma unroll
+        for (int k = 0; k < K::NS; ++k) row[K::NA + k] = active ? B[k] : R(__longlong_as_double(0x7ff8000000000000ll));
+        if (w == 1) {
+          RowIO<R, DSO>::store_major(out_a, tid, row);
+        } else {
+          RowIO<R, DSO>::store_interleaved(out_a, tid, w, row);
+        }
+      }
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (tid == 0) {
+        const unsigned ob = padded * DSO * sizeof(R);
+        char *go = static_cast<char *>(p.stiffness) + e0 * DSO * sizeof(R);
+        const unsigned ob16 = ob & ~15u;
+        if (ob16) bulk_store(go, out_a, ob16);
+        bulk_commit();
+        for (unsigned k = ob16; k < ob; k += 4) *reinterpret_cast<uint32_t *>(go + k) = lds32(out_a + k);
+      }
+      continue;
+    }
     if (active) {
       RowIO<R, K::NA>::store_major(out_a, tid, A);
       RowIO<R, K::NS>::store_major(out_b, tid, B);

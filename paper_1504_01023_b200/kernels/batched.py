@@ -77,10 +77,31 @@ class BatchResult:
     load: object
     traffic: TrafficCounters
     out_layout: BatchLayout = field(default=ELEMENT_MAJOR)
+    # packed rows [A | b] in out_layout, written by the kernel (integrate_batch(..., packed=True));
+    # stiffness/load are then zero-copy views (element-major) or None (interleaved)
+    flat: object = None
+
+    def _materialize(self) -> None:
+        """Unpack stiffness/load from kernel-packed interleaved rows on first use."""
+        if self.stiffness is not None or self.flat is None:
+            return
+        ns = self.descriptor.element.n_shape
+        ds, n = ns * ns + ns, self.n_elements
+        layout = coerce_layout(self.out_layout)
+        if _is_torch(self.flat):
+            w = layout.lane_width
+            rows = self.flat.view(-1, ds, w).transpose(1, 2).reshape(-1, ds)[:n].contiguous()
+        else:
+            from ..layout import unpack_rows
+
+            rows = unpack_rows(self.flat, n, ds, layout)
+        self.stiffness = rows[:, : ns * ns].reshape(n, ns, ns)
+        self.load = rows[:, ns * ns:]
 
     def element_matrix(self, e: int) -> ElementMatrix:
         if not 0 <= e < self.n_elements:
             raise IndexError(f"element index {e} out of range")
+        self._materialize()
         A, b = self.stiffness[e], self.load[e]
         if _is_torch(A):
             A, b = A.detach().cpu().numpy(), b.detach().cpu().numpy()
@@ -88,6 +109,7 @@ class BatchResult:
 
     def output_rows(self):
         """(n, ns*ns + ns) rows: stiffness entries then load (``batched.py:99-102``)."""
+        self._materialize()
         n = self.n_elements
         if _is_torch(self.stiffness):
             import torch
@@ -96,9 +118,24 @@ class BatchResult:
         return np.concatenate([np.asarray(self.stiffness).reshape(n, -1), np.asarray(self.load)], axis=1)
 
     def flat_output(self, pad_value: float = np.nan):
-        """Rows flattened in ``out_layout`` (``batched.py:104-106``); stays on the device for device results."""
-        rows = self.output_rows()
+        """Rows flattened in ``out_layout`` (``batched.py:104-106``); stays on the device for device results.
+
+        For kernel-packed results (``packed=True``) this is the kernel's own
+        output buffer (no repacking pass); pad lanes hold NaN unless another
+        ``pad_value`` is requested.
+        """
         layout = coerce_layout(self.out_layout)
+        if self.flat is not None:
+            if layout.kind is LayoutKind.ELEMENT_MAJOR or self.n_elements % layout.lane_width == 0 \
+                    or np.isnan(pad_value):
+                return self.flat
+            out = self.flat.clone() if _is_torch(self.flat) else self.flat.copy()
+            ds = self.descriptor.element.n_shape * (self.descriptor.element.n_shape + 1)
+            w, n = layout.lane_width, self.n_elements
+            blk = out.reshape(-1, ds, w)
+            blk[-1, :, n % w:] = pad_value
+            return out
+        rows = self.output_rows()
         if not _is_torch(rows):
             return pack_rows(rows, layout, pad_value)
         import torch
@@ -115,6 +152,7 @@ class BatchResult:
         return out
 
     def to_host(self) -> "BatchResult":
+        self._materialize()
         if not _is_torch(self.stiffness):
             return self
         return BatchResult(self.descriptor, self.n_elements, self.stiffness.cpu().numpy(),
@@ -176,7 +214,9 @@ class DeviceBatch:
 # ---------------------------------------------------------------------------
 
 def _desc_struct(desc: KernelDescriptor, layout: BatchLayout, n: int, base: int, dtype_code: int,
-                 geometry: int, coefficients: int, stiffness: int, load: int, error_key: int) -> _native.BatchDesc:
+                 geometry: int, coefficients: int, stiffness: int, load: int, error_key: int,
+                 out_layout: BatchLayout | None = None) -> _native.BatchDesc:
+    """C descriptor; ``out_layout`` set -> packed output rows in that layout."""
     d = _native.BatchDesc()
     d.element = _native.ELEMENT[desc.element.value]
     d.problem = _native.PROBLEM[desc.problem.value]
@@ -189,6 +229,11 @@ def _desc_struct(desc: KernelDescriptor, layout: BatchLayout, n: int, base: int,
     d.base_index = base
     d.geometry, d.coefficients = geometry, coefficients
     d.stiffness, d.load, d.error_key = stiffness, load, error_key
+    if out_layout is None:
+        d.out_format, d.out_lane_width = _native.OUT_SPLIT, 1
+    else:
+        d.out_format = _native.OUT_PACKED
+        d.out_lane_width = out_layout.lane_width if out_layout.kind is LayoutKind.LANE_INTERLEAVED else 1
     return d
 
 
@@ -232,30 +277,50 @@ def _device_error_detail(dd: _native.BatchDesc, local: int, point, stream) -> tu
     return det, tol
 
 
+def _packed_views(flat, n: int, ns: int, out_layout: BatchLayout):
+    """(stiffness, load) zero-copy views of element-major packed rows, else (None, None)."""
+    if out_layout.kind is LayoutKind.LANE_INTERLEAVED and out_layout.lane_width > 1:
+        return None, None
+    rows = flat.reshape(n, ns * ns + ns)
+    A, b = rows[:, : ns * ns], rows[:, ns * ns:]
+    if _is_torch(A):
+        return A.unflatten(1, (ns, ns)), b
+    return A.reshape(n, ns, ns), b
+
+
 # ---------------------------------------------------------------------------
 # device path
 # ---------------------------------------------------------------------------
 
 def _integrate_device(desc: KernelDescriptor, batch: DeviceBatch, out_layout, check: bool, base_index: int,
-                      out=None) -> BatchResult:
+                      out=None, packed: bool = False) -> BatchResult:
     import torch
 
     lib = _native.load()
     n, ns = batch.n_elements, desc.element.n_shape
     dev = batch.geometry_data.device
     dtype_code = _native.DTYPE["float64" if batch.dtype == torch.float64 else "float32"]
-    if out is None:
-        A = torch.empty((n, ns, ns), dtype=batch.dtype, device=dev)
-        b = torch.empty((n, ns), dtype=batch.dtype, device=dev)
+    olayout = coerce_layout(out_layout)
+    flat = None
+    if packed:
+        flat = torch.empty(flat_length(n, ns * ns + ns, olayout), dtype=batch.dtype, device=dev)
+        A, b = _packed_views(flat, n, ns, olayout)
+        ptr_a, ptr_b = flat.data_ptr(), 0
     else:
-        A, b = out
+        if out is None:
+            A = torch.empty((n, ns, ns), dtype=batch.dtype, device=dev)
+            b = torch.empty((n, ns), dtype=batch.dtype, device=dev)
+        else:
+            A, b = out
+        ptr_a, ptr_b = A.data_ptr(), b.data_ptr()
     err = torch.full((1,), -1, dtype=torch.int64, device=dev)
     dd = _desc_struct(desc, batch.layout, n, base_index, dtype_code, batch.geometry_data.data_ptr(),
-                      batch.coefficient_data.data_ptr(), A.data_ptr(), b.data_ptr(), err.data_ptr())
+                      batch.coefficient_data.data_ptr(), ptr_a, ptr_b, err.data_ptr(),
+                      out_layout=olayout if packed else None)
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream().cuda_stream
         _native.check(lib.fek_integrate(ctypes.byref(dd), stream), "fek_integrate")
-        result = BatchResult(desc, n, A, b, _traffic(desc, n), coerce_layout(out_layout))
+        result = BatchResult(desc, n, A, b, _traffic(desc, n), olayout, flat)
         result.error_word = err
         if check:
             key = int(err.item()) & _native.NO_ERROR
@@ -296,7 +361,7 @@ def _aligned_f64(a) -> np.ndarray:
     return a
 
 
-def _integrate_host(desc: KernelDescriptor, batch, out_layout, base_index: int) -> BatchResult:
+def _integrate_host(desc: KernelDescriptor, batch, out_layout, base_index: int, packed: bool = False) -> BatchResult:
     import torch
 
     if not torch.cuda.is_available():
@@ -306,10 +371,18 @@ def _integrate_host(desc: KernelDescriptor, batch, out_layout, base_index: int) 
     n, ns = int(batch.n_elements), desc.element.n_shape
     geo = _aligned_f64(batch.geometry_data)
     cof = _aligned_f64(batch.coefficient_data)
-    A = hostmem.empty((n, ns, ns))
-    b = hostmem.empty((n, ns))
+    olayout = coerce_layout(out_layout)
+    flat = None
+    if packed:
+        flat = hostmem.empty(flat_length(n, ns * ns + ns, olayout))
+        A, b = _packed_views(flat, n, ns, olayout)
+        ptr_a, ptr_b = flat.ctypes.data, 0
+    else:
+        A = hostmem.empty((n, ns, ns))
+        b = hostmem.empty((n, ns))
+        ptr_a, ptr_b = A.ctypes.data, b.ctypes.data
     dd = _desc_struct(desc, layout, n, base_index, _native.DTYPE["float64"], geo.ctypes.data, cof.ctypes.data,
-                      A.ctypes.data, b.ctypes.data, 0)
+                      ptr_a, ptr_b, 0, out_layout=olayout if packed else None)
     device = torch.cuda.current_device()
     streams = _host_streams(device)
     chunk = host_chunk_elements(n)
@@ -338,7 +411,7 @@ def _integrate_host(desc: KernelDescriptor, batch, out_layout, base_index: int) 
 
         _raise_geometry(key.value, detail)
     _native.check(status, "fek_integrate_host")
-    return BatchResult(desc, n, A, b, _traffic(desc, n), coerce_layout(out_layout))
+    return BatchResult(desc, n, A, b, _traffic(desc, n), olayout, flat)
 
 
 # ---------------------------------------------------------------------------
@@ -346,24 +419,26 @@ def _integrate_host(desc: KernelDescriptor, batch, out_layout, base_index: int) 
 # ---------------------------------------------------------------------------
 
 def integrate_batch(desc, batch, out_layout: BatchLayout = ELEMENT_MAJOR, workers: int = 1, *,
-                    check: bool = True, base_index: int = 0, out=None) -> BatchResult:
+                    check: bool = True, base_index: int = 0, out=None, packed: bool = False) -> BatchResult:
     """Integrate every element of ``batch`` with the kernel named by ``desc``.
 
     Mirrors ``feklab.kernels.integrate_batch`` (``batched.py:536-606``).
     Extra keyword-only knobs: ``check=False`` skips the device->host read of
     the error word for device batches (``result.error_word`` holds it);
     ``base_index`` offsets reported element indices (sharded batches);
-    ``out=(A, b)`` supplies preallocated device outputs.
+    ``out=(A, b)`` supplies preallocated device outputs; ``packed=True`` has
+    the kernel write ``flat_output()``'s packed rows in ``out_layout``
+    directly (``result.flat``; no repacking pass).
     """
     desc = coerce_descriptor(desc)
     _check_match(desc, batch)
     if int(workers) < 1:
         workers = 1
     if isinstance(batch, DeviceBatch):
-        return _integrate_device(desc, batch, out_layout, check, base_index, out)
+        return _integrate_device(desc, batch, out_layout, check, base_index, out, packed)
     if _is_torch(getattr(batch, "geometry_data", None)):
         raise TypeError("batches of torch tensors must be wrapped in DeviceBatch")
-    return _integrate_host(desc, batch, out_layout, base_index)
+    return _integrate_host(desc, batch, out_layout, base_index, packed)
 
 
 def launch_config(desc, layout: BatchLayout, n: int, dtype: str = "float64") -> dict:
