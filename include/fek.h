@@ -96,7 +96,8 @@ typedef struct fek_batch_desc {
   void *load;             /* SPLIT: (n, ns) reals.  PACKED: unused (NULL)         */
   unsigned long long *error_key; /* device word (fek_integrate), init FEK_NO_ERROR */
   int32_t out_lane_width; /* PACKED: output lane width W (1 = element-major rows)  */
-  int32_t reserved;
+  int32_t ctas_per_sm;    /* cap on resident CTAs per SM for this launch (0 = occupancy
+                             maximum); lets two launches share the SMs concurrently  */
 } fek_batch_desc;
 
 int fek_abi_version(void);

@@ -53,7 +53,7 @@ class BatchDesc(ctypes.Structure):
         ("load", ctypes.c_void_p),
         ("error_key", ctypes.c_void_p),
         ("out_lane_width", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("ctas_per_sm", ctypes.c_int32),
     ]
 
 

@@ -96,7 +96,7 @@ int validate(const fek_batch_desc *d, bool need_pointers) {
   } else {
     return FEK_ERR_ARGUMENT;
   }
-  if (d->n_elements < 0 || d->base_index < 0) return FEK_ERR_ARGUMENT;
+  if (d->n_elements < 0 || d->base_index < 0 || d->ctas_per_sm < 0) return FEK_ERR_ARGUMENT;
   const bool packed = d->out_format == FEK_OUT_PACKED;
   if (!packed && d->out_format != FEK_OUT_SPLIT) return FEK_ERR_ARGUMENT;
   if (packed) {
@@ -120,7 +120,8 @@ int launch(const fek_batch_desc *d, cudaStream_t stream, int *grid_out, int *blo
   LaunchGeometry lg;
   if (int rc = launch_geometry(idx, ke, &lg)) return rc;
   const long long tiles = (d->n_elements + ke.tile - 1) / ke.tile;
-  const long long cap = static_cast<long long>(lg.sms) * lg.resident;
+  const int per_sm = (d->ctas_per_sm > 0 && d->ctas_per_sm < lg.resident) ? d->ctas_per_sm : lg.resident;
+  const long long cap = static_cast<long long>(lg.sms) * per_sm;
   const int grid = static_cast<int>(tiles < cap ? tiles : cap);
   if (grid_out) *grid_out = grid;
   if (block_out) *block_out = ke.threads;

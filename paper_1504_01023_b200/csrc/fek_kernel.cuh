@@ -55,7 +55,7 @@ struct Traits {
   static constexpr int DSC = (PB == POISSON) ? NQ : 20;
   static constexpr int NA = NS * NS;
   static constexpr int THREADS = 128;
-  static constexpr int TILE = 128;
+  static constexpr int TILE = THREADS;
   // prisms (and the re-computing generic variants) re-read coordinates from
   // the staged tile instead of pinning 18 reals in registers
   static constexpr bool LAZY_X = (GEO == GEO_GENERIC) && (ET == PRISM || VAR != QSS);
