@@ -30,7 +30,9 @@ _STATE = {}
 def _shared(shape) -> np.ndarray:
     size = int(np.prod(shape)) * 8
     buf = mmap.mmap(-1, max(size, 8))
-    return np.frombuffer(buf, dtype=np.float64, count=int(np.prod(shape))).reshape(shape)
+    arr = np.frombuffer(buf, dtype=np.float64, count=int(np.prod(shape))).reshape(shape)
+    arr.fill(0.0)  # fault the pages in before forking, so timed runs measure compute only
+    return arr
 
 
 def _work(args):
