@@ -126,9 +126,8 @@ def run_reference(args) -> int:
         with PortPool(desc.variant.value, desc.geometry_path.value, pb.value, et.value, geo, cof, procs) as pool:
             for _ in range(max(args.warmup, 1)):
                 pool.run(0, part)  # full-size warm-up: worker heaps / page tables populated
-            for k in range(args.steps):
-                lo = (k * part) % max(1, n - part + 1)
-                times.append(pool.run(lo, lo + part))
+            for _ in range(args.steps):  # same window every step, as the reference's bench repeats its batch
+                times.append(pool.run(0, part))
         sec += float(np.mean(times))
         sample += part
     cfg = mesh.bench_configs()[keys[0]]
