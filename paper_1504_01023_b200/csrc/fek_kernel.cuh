@@ -126,6 +126,7 @@ struct Pipe {
     if (gb & ~15u) bulk_load(geo(s), gsrc, gb & ~15u, full(s), policy);
     if (cb & ~15u) bulk_load(coef(s), csrc, cb & ~15u, full(s), policy);
   }
+
 };
 
 template <class K>
@@ -153,7 +154,10 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
     const int s = i % K::STAGES;
     const bool landed = mbar_wait(pipe.full(s), (i / K::STAGES) & 1);
     if (__syncthreads_or(!landed)) {
-      if (tid == 0) atomicMin(p.error_key, static_cast<unsigned long long>(KIND_PIPELINE_TIMEOUT));
+      if (tid == 0) {
+        atomicMin(p.error_key, static_cast<unsigned long long>(KIND_PIPELINE_TIMEOUT));
+        bulk_wait_all<0>();  // no bulk store may still be reading smem at exit
+      }
       return;
     }
     const long long e0 = t * K::TILE;
