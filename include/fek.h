@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define FEK_ABI_VERSION 2
+#define FEK_ABI_VERSION 3
 
 /* enums mirror the Python ones (refelem.py:29, problems.py:26-49) */
 enum fek_element { FEK_TETRAHEDRON = 0, FEK_PRISM = 1 };
@@ -98,6 +98,13 @@ typedef struct fek_batch_desc {
   int32_t out_lane_width; /* PACKED: output lane width W (1 = element-major rows)  */
   int32_t ctas_per_sm;    /* cap on resident CTAs per SM for this launch (0 = occupancy
                              maximum); lets two launches share the SMs concurrently  */
+  unsigned long long *scheduler; /* optional device words [2], zero-initialised once:
+                             dynamic tile queue (CTAs take tiles with atomicAdd, the
+                             last CTA resets both words, so a buffer is reusable by
+                             later launches on the same stream; one buffer per
+                             concurrently running launch).  NULL = static
+                             round-robin tiles.  fek_integrate_host ignores it
+                             and keeps one queue per stream in its workspace. */
 } fek_batch_desc;
 
 int fek_abi_version(void);

@@ -19,7 +19,7 @@ if os.environ.get("FEK_LIB_OVERRIDE"):  # kernel-tuning experiments only
     LIB_PATH = os.path.abspath(os.environ["FEK_LIB_OVERRIDE"])
 HEADER_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "fek.h")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 NO_ERROR = 0xFFFFFFFFFFFFFFFF
 
 OK, ERR_ARGUMENT, ERR_ALIGNMENT, ERR_CUDA, ERR_WORKSPACE, ERR_GEOMETRY = range(6)
@@ -54,6 +54,7 @@ class BatchDesc(ctypes.Structure):
         ("error_key", ctypes.c_void_p),
         ("out_lane_width", ctypes.c_int32),
         ("ctas_per_sm", ctypes.c_int32),
+        ("scheduler", ctypes.c_void_p),
     ]
 
 

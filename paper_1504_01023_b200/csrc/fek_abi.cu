@@ -108,6 +108,7 @@ int validate(const fek_batch_desc *d, bool need_pointers) {
     if (!aligned16(d->geometry) || !aligned16(d->coefficients) || !aligned16(d->stiffness) ||
         (!packed && !aligned16(d->load)))
       return FEK_ERR_ALIGNMENT;
+    if (reinterpret_cast<uintptr_t>(d->scheduler) % 8) return FEK_ERR_ALIGNMENT;
   }
   return FEK_OK;
 }
@@ -139,6 +140,7 @@ int launch(const fek_batch_desc *d, cudaStream_t stream, int *grid_out, int *blo
   p.lane_width = d->layout == FEK_ELEMENT_MAJOR ? 1 : d->lane_width;
   p.out_packed = d->out_format == FEK_OUT_PACKED;
   p.out_width = p.out_packed ? d->out_lane_width : 1;
+  p.scheduler = d->scheduler;
   ke.fn<<<grid, ke.threads, ke.smem, stream>>>(p);
   FEK_CUDA(cudaGetLastError());
   return FEK_OK;
@@ -317,6 +319,8 @@ struct SlotPlan {
 };
 
 size_t round256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
+// workspace header: the error word, then one [2]-word tile queue per stream slot
+size_t host_header_bytes(int n_streams) { return round256(16 + 16 * static_cast<size_t>(n_streams)); }
 
 SlotPlan slot_plan(const fek_batch_desc *d, long long chunk) {
   const size_t rb = real_bytes(d->dtype);
@@ -335,7 +339,7 @@ long long flat_len(long long n, int ds, int w) { return n == 0 ? 0 : ((n + w - 1
 
 size_t fek_host_workspace_bytes(const fek_batch_desc *d, int n_streams, int64_t chunk_elements) {
   if (!d || n_streams < 1 || chunk_elements < 1) return 0;
-  return 256 + static_cast<size_t>(n_streams) * slot_plan(d, chunk_elements).slot;
+  return host_header_bytes(n_streams) + static_cast<size_t>(n_streams) * slot_plan(d, chunk_elements).slot;
 }
 
 int fek_integrate_host(const fek_batch_desc *d, void *device_workspace, size_t workspace_bytes, int n_streams,
@@ -363,8 +367,12 @@ int fek_integrate_host(const fek_batch_desc *d, void *device_workspace, size_t w
   const int ns = n_shape(d->element);
   cudaStream_t s0 = static_cast<cudaStream_t>(cuda_streams[0]);
 
-  // error word initialised on stream 0; the other streams wait for it
+  unsigned long long *queues = reinterpret_cast<unsigned long long *>(ws + 16);
+  const size_t header = host_header_bytes(n_streams);
+
+  // error word and tile queues initialised on stream 0; the other streams wait for it
   FEK_CUDA(cudaMemsetAsync(dkey, 0xFF, sizeof(unsigned long long), s0));
+  FEK_CUDA(cudaMemsetAsync(queues, 0, 16 * static_cast<size_t>(n_streams), s0));
   cudaEvent_t ready;
   FEK_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   FEK_CUDA(cudaEventRecord(ready, s0));
@@ -381,7 +389,7 @@ int fek_integrate_host(const fek_batch_desc *d, void *device_workspace, size_t w
     const long long cnt = (n - lo) < chunk ? (n - lo) : chunk;
     const int slot = static_cast<int>(ci % n_streams);
     cudaStream_t st = static_cast<cudaStream_t>(cuda_streams[slot]);
-    char *base = ws + 256 + slot * sp.slot;
+    char *base = ws + header + slot * sp.slot;
     char *dg = base, *dc = base + sp.geo, *dA = dc + sp.coef, *db = dA + sp.A;
     // lo is a multiple of 128 (hence of W): the chunk's flat range starts at lo*DS
     const size_t gbytes = flat_len(cnt, dsg, w) * rb, cbytes = flat_len(cnt, dsc, w) * rb;
@@ -399,6 +407,7 @@ int fek_integrate_host(const fek_batch_desc *d, void *device_workspace, size_t w
     cd.stiffness = dA;
     cd.load = db;
     cd.error_key = dkey;
+    cd.scheduler = queues + 2 * slot;  // launches on one stream are ordered: one queue per slot
     rc = launch(&cd, st, nullptr, nullptr, nullptr, nullptr, true);
     if (rc) break;
     if (d->out_format == FEK_OUT_PACKED) {

@@ -43,6 +43,7 @@ struct LaunchParams {
   int lane_width;
   int out_packed;  // FEK_OUT_PACKED: rows [A | b] into `stiffness` in the output layout
   int out_width;   // output lane width (1 = element-major rows)
+  unsigned long long *scheduler;  // [next tile, CTAs done] or null (static round-robin)
 };
 
 template <typename R_, int ET_, int PB_, int VAR_, int GEO_>
@@ -146,25 +147,47 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
     fence_mbar_init();
   }
   __syncthreads();
+  // Tile sources: static round-robin (blockIdx.x + i*gridDim.x), or a dynamic
+  // queue (atomicAdd on scheduler[0]) so CTAs that start late -- e.g. while
+  // another launch holds part of the SM -- simply take fewer tiles.  Thread 0
+  // records each stage's tile in smem before arriving on the stage barrier, so
+  // consumers read it after the wait; tiles past the end arrive without bytes.
+  __shared__ long long s_tile[K::STAGES];
+  long long static_next = blockIdx.x;
+  auto issue_stage = [&](int s) {
+    long long t;
+    if (p.scheduler) {
+      t = static_cast<long long>(atomicAdd(p.scheduler, 1ull));
+    } else {
+      t = static_next;
+      static_next += gridDim.x;
+    }
+    s_tile[s] = t;
+    if (t < pipe.tiles) {
+      pipe.issue(p, t, s);
+    } else {
+      mbar_arrive(pipe.full(s));
+    }
+  };
   if (tid == 0)
-    for (int s = 0; s < K::STAGES; ++s) pipe.issue(p, blockIdx.x + static_cast<long long>(s) * gridDim.x, s);
+    for (int s = 0; s < K::STAGES; ++s) issue_stage(s);
 
-  int i = 0;
-  for (long long t = blockIdx.x; t < pipe.tiles; t += gridDim.x, ++i) {
+  for (int i = 0;; ++i) {
     const int s = i % K::STAGES;
     const bool landed = mbar_wait(pipe.full(s), (i / K::STAGES) & 1);
     if (__syncthreads_or(!landed)) {
-      if (tid == 0) {
-        atomicMin(p.error_key, static_cast<unsigned long long>(KIND_PIPELINE_TIMEOUT));
-        bulk_wait_all<0>();  // no bulk store may still be reading smem at exit
-      }
-      return;
+      // report and leave through the common exit (drains bulk stores, retires the queue)
+      if (tid == 0) atomicMin(p.error_key, static_cast<unsigned long long>(KIND_PIPELINE_TIMEOUT));
+      break;
     }
+    // tiles are taken in increasing order per CTA, so the first stage past the
+    // end means every later stage is past the end too (nothing in flight)
+    const long long t = *static_cast<volatile long long *>(&s_tile[s]);
+    if (t >= pipe.tiles) break;
     const long long e0 = t * K::TILE;
     const int count = static_cast<int>(min(static_cast<long long>(K::TILE), p.n - e0));
     const bool active = tid < count;
     const long long e_abs = p.base + e0 + tid;
-    const long long tn = t + static_cast<long long>(K::STAGES) * gridDim.x;
     R C[K::DSC];
     R A[K::NA];
     R B[K::NS];
@@ -176,7 +199,7 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
         RowIO<R, K::DSC>::load(pipe.coef(s), tid, p.lane_width, C);
       }
       __syncthreads();
-      if (tid == 0) pipe.issue(p, tn, s);
+      if (tid == 0) issue_stage(s);
       if (active) {
         if constexpr (K::GEO == GEO_LINEAR) {
           integrate_tet_linear<R, K::PB>(X, C, A, B, kind);
@@ -197,7 +220,7 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
                                                    kind_point);
       }
       __syncthreads();
-      if (tid == 0) pipe.issue(p, tn, s);
+      if (tid == 0) issue_stage(s);
     }
     if (kind) atomicMin(p.error_key, make_error_key(e_abs, kind_point, kind));
     if (tid == 0) bulk_wait_read<0>();
@@ -251,7 +274,17 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
       for (unsigned k = bb16; k < bb; k += 4) *reinterpret_cast<uint32_t *>(gb + k) = lds32(out_b + k);
     }
   }
-  if (tid == 0) bulk_wait_all<0>();
+  if (tid == 0) {
+    bulk_wait_all<0>();  // no bulk store may still be reading smem at exit
+    if (p.scheduler) {
+      // the last CTA out resets the queue for the next launch on this buffer
+      __threadfence();
+      if (atomicAdd(p.scheduler + 1, 1ull) == gridDim.x - 1ull) {
+        atomicExch(p.scheduler, 0ull);
+        atomicExch(p.scheduler + 1, 0ull);
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------

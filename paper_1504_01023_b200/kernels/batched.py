@@ -292,6 +292,24 @@ def _packed_views(flat, n: int, ns: int, out_layout: BatchLayout):
 # device path
 # ---------------------------------------------------------------------------
 
+_QUEUES: dict = {}
+
+
+def _tile_queue(dev, stream: int):
+    """Two zeroed int64 words per (device, stream): the kernel's dynamic tile queue.
+
+    Launches on one stream run in order and the last CTA of each launch resets
+    the words, so one buffer serves every launch on that stream.
+    """
+    import torch
+
+    key = (dev.index, stream)
+    q = _QUEUES.get(key)
+    if q is None:
+        q = _QUEUES[key] = torch.zeros(2, dtype=torch.int64, device=dev)
+    return q
+
+
 def _integrate_device(desc: KernelDescriptor, batch: DeviceBatch, out_layout, check: bool, base_index: int,
                       out=None, packed: bool = False) -> BatchResult:
     import torch
@@ -319,6 +337,7 @@ def _integrate_device(desc: KernelDescriptor, batch: DeviceBatch, out_layout, ch
                       out_layout=olayout if packed else None)
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream().cuda_stream
+        dd.scheduler = _tile_queue(dev, stream).data_ptr()
         _native.check(lib.fek_integrate(ctypes.byref(dd), stream), "fek_integrate")
         result = BatchResult(desc, n, A, b, _traffic(desc, n), olayout, flat)
         result.error_word = err
