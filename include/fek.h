@@ -172,6 +172,18 @@ int fek_mesh_geometry(int32_t element, int64_t nx, int64_t ny, int64_t nz, int64
                       const unsigned long long *jitter_stream, double jitter_amplitude, double *out,
                       void *cuda_stream);
 
+/* ---- on-device layout conversion -----------------
+ * Replaces layout.convert / pack_rows / unpack_rows
+ * (pkg/src/feklab/layout.py:72-94,174-183) for arrays already in HBM:
+ * n_elements rows of row_size reals (dtype FEK_F64 / FEK_F32, row_size
+ * <= 42) stored with lane width in_lane_width (1 = element-major) are
+ * rewritten into dst with lane width out_lane_width; pad lanes of a partial
+ * interleaved output block get pad_value (NaN = the reference's default).
+ * dst holds ceil(n / W_out) * W_out * row_size reals and must not overlap
+ * src.  Asynchronous on cuda_stream. */
+int fek_convert_layout(const void *src, int32_t in_lane_width, void *dst, int32_t out_lane_width, int64_t n_elements,
+                       int32_t row_size, int32_t dtype, double pad_value, void *cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -81,6 +81,8 @@ SIGNATURES = {
     "fek_mesh_geometry": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                          ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_ulonglong),
                                          ctypes.c_double, _P, _P]),
+    "fek_convert_layout": (ctypes.c_int, [_P, ctypes.c_int32, _P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,
+                                          ctypes.c_int32, ctypes.c_double, _P]),
 }
 
 _lib = None

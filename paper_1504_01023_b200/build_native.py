@@ -46,7 +46,7 @@ def _nvcc() -> str:
 
 
 def _sources() -> list[str]:
-    return [os.path.join(CSRC, "fek_abi.cu"), os.path.join(CSRC, "fek_mesh.cu")] + sorted(
+    return [os.path.join(CSRC, n) for n in ("fek_abi.cu", "fek_mesh.cu", "fek_layout.cu")] + sorted(
         glob.glob(os.path.join(CSRC, "cases", "*.cu")))
 
 

@@ -8,6 +8,16 @@
 
 #include "../../include/fek.h"
 #include "fek_dispatch.cuh"
+#include "fek_status.h"
+
+namespace {
+thread_local char g_cuda_error[256] = "";
+}  // namespace
+
+int fek::record_cuda_error(cudaError_t e, const char *what) {
+  std::snprintf(g_cuda_error, sizeof(g_cuda_error), "%s: %s", what, cudaGetErrorString(e));
+  return FEK_ERR_CUDA;
+}
 
 namespace {
 
@@ -16,12 +26,7 @@ using fek::kIndexCount;
 using fek::kernel_index;
 using fek::LaunchParams;
 
-thread_local char g_cuda_error[256] = "";
-
-int cuda_fail(cudaError_t e, const char *what) {
-  std::snprintf(g_cuda_error, sizeof(g_cuda_error), "%s: %s", what, cudaGetErrorString(e));
-  return FEK_ERR_CUDA;
-}
+int cuda_fail(cudaError_t e, const char *what) { return fek::record_cuda_error(e, what); }
 
 #define FEK_CUDA(call)                              \
   do {                                              \

@@ -14,6 +14,7 @@
 #include <cstdio>
 
 #include "../../include/fek.h"
+#include "fek_status.h"
 
 namespace {
 
@@ -147,13 +148,7 @@ __global__ void prism_rows_kernel(long long nx, long long ny, long long first, l
   }
 }
 
-thread_local char g_err[160] = "";
-
-int cuda_status(cudaError_t e) {
-  if (e == cudaSuccess) return FEK_OK;
-  snprintf(g_err, sizeof(g_err), "%s", cudaGetErrorString(e));
-  return FEK_ERR_CUDA;
-}
+int cuda_status(cudaError_t e) { return e == cudaSuccess ? FEK_OK : fek::record_cuda_error(e, "fek_mesh launch"); }
 
 }  // namespace
 

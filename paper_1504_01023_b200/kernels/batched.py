@@ -31,7 +31,7 @@ import numpy as np
 
 from .. import _native, hostmem
 from ..errors import DegenerateElement, InvertedElement, NativeLibraryError, ShapeMismatch
-from ..layout import ELEMENT_MAJOR, BatchLayout, LayoutKind, coerce_layout, flat_length, pack_rows
+from ..layout import ELEMENT_MAJOR, BatchLayout, ElementBatch, LayoutKind, coerce_layout, flat_length, pack_rows
 from ..problems import (ElementMatrix, KernelDescriptor, ProblemClass, coerce_descriptor, coerce_element,
                         coerce_problem)
 from ..refelem import ElementType
@@ -207,6 +207,41 @@ class DeviceBatch:
 
         return cls(coerce_element(batch.element_type), coerce_problem(batch.problem), int(batch.n_elements),
                    coerce_layout(batch.layout), up(batch.geometry_data), up(batch.coefficient_data))
+
+    def convert(self, to: BatchLayout, pad_value: float = np.nan) -> "DeviceBatch":
+        """On-device ``layout.convert`` (``layout.py:198-218``): a new batch in layout ``to``.
+
+        The same layout returns copies, as the reference does; otherwise both
+        arrays are repacked by ``fek_convert_layout`` with ``pad_value`` in the
+        pad lanes of a partial interleaved block.
+        """
+        import torch
+
+        to = coerce_layout(to)
+        if to == self.layout:
+            return DeviceBatch(self.element_type, self.problem, self.n_elements, self.layout,
+                               self.geometry_data.clone(), self.coefficient_data.clone())
+        lib = _native.load()
+        dtype = _native.DTYPE["float64" if self.dtype == torch.float64 else "float32"]
+        w_in, w_out = self.layout.block, to.block
+        out = []
+        with torch.cuda.device(self.geometry_data.device):
+            stream = torch.cuda.current_stream().cuda_stream
+            for src, ds in ((self.geometry_data, self.element_type.geometry_size),
+                            (self.coefficient_data, self.problem.coefficient_size(self.element_type))):
+                dst = torch.empty(flat_length(self.n_elements, ds, to), dtype=src.dtype, device=src.device)
+                _native.check(lib.fek_convert_layout(src.data_ptr(), w_in, dst.data_ptr(), w_out, self.n_elements,
+                                                     ds, dtype, float(pad_value), stream), "fek_convert_layout")
+                out.append(dst)
+        return DeviceBatch(self.element_type, self.problem, self.n_elements, to, *out)
+
+    def to_host(self) -> ElementBatch:
+        """Download as a float64 host ``ElementBatch`` in the same layout."""
+        import torch
+
+        geo = self.geometry_data.to(torch.float64).cpu().numpy()
+        cof = self.coefficient_data.to(torch.float64).cpu().numpy()
+        return ElementBatch(self.element_type, self.problem, self.n_elements, self.layout, geo, cof)
 
 
 # ---------------------------------------------------------------------------
