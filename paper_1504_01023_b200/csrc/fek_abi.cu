@@ -324,6 +324,21 @@ struct SlotPlan {
 };
 
 size_t round256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
+// Chunk ci of the host pipeline, `rem` elements left, `chunk` the slot size.
+// The first chunks ramp up (chunk/8, /4, /2) so the device-to-host engine
+// starts early, and the last ones halve what is left down to chunk/8 so the
+// final kernel + download (the only part nothing overlaps) is short.
+// Multiples of `align` except the very last piece.
+long long pipeline_chunk(long long ci, long long rem, long long chunk, long long align) {
+  const long long floor_size = ((chunk / 8 + align - 1) / align) * align;
+  long long size = ci < 3 ? (chunk >> (3 - ci)) : chunk;
+  const long long half = (((rem + 1) / 2 + align - 1) / align) * align;
+  if (half < size) size = half;
+  if (size < floor_size) size = floor_size;
+  size = ((size + align - 1) / align) * align;
+  return size < rem ? size : rem;
+}
+
 // workspace header: the error word, then one [2]-word tile queue per stream slot
 size_t host_header_bytes(int n_streams) { return round256(16 + 16 * static_cast<size_t>(n_streams)); }
 
@@ -390,8 +405,9 @@ int fek_integrate_host(const fek_batch_desc *d, void *device_workspace, size_t w
   char *hb = static_cast<char *>(d->load);
   int rc = FEK_OK;
   long long ci = 0;
-  for (long long lo = 0; lo < n && rc == FEK_OK; lo += chunk, ++ci) {
-    const long long cnt = (n - lo) < chunk ? (n - lo) : chunk;
+  long long cnt = 0;
+  for (long long lo = 0; lo < n && rc == FEK_OK; lo += cnt, ++ci) {
+    cnt = pipeline_chunk(ci, n - lo, chunk, align);
     const int slot = static_cast<int>(ci % n_streams);
     cudaStream_t st = static_cast<cudaStream_t>(cuda_streams[slot]);
     char *base = ws + header + slot * sp.slot;
