@@ -82,3 +82,26 @@ def test_convert_argument_errors():
     assert lib.fek_convert_layout(None, 3, None, 1, 10, 12, 0, 0.0, None) == _native.ERR_ARGUMENT
     assert lib.fek_convert_layout(None, 1, None, 1, 10, 43, 0, 0.0, None) == _native.ERR_ARGUMENT
     assert lib.fek_convert_layout(None, 1, None, 1, 0, 12, 0, 0.0, None) == _native.OK
+
+
+def test_convert_unaligned_arrays_take_the_plain_kernel():
+    """Arrays offset by one fp32 word (not 16-byte aligned) use the plain-load kernel: same bytes."""
+    import torch
+
+    hb = host_batch(ElementType.PRISM, ProblemClass.POISSON, 1001, 4)
+    db = DeviceBatch.from_host(hb, dtype=torch.float32)
+
+    def shifted(t):
+        buf = torch.empty(t.numel() + 1, dtype=t.dtype, device=t.device)
+        view = buf[1:]
+        view.copy_(t)
+        return view
+
+    odd = DeviceBatch(db.element_type, db.problem, db.n_elements, db.layout,
+                      shifted(db.geometry_data), shifted(db.coefficient_data))
+    assert odd.geometry_data.data_ptr() % 16 != 0
+    for w in (1, 16):
+        a, b = odd.convert(lay(w)), db.convert(lay(w))
+        assert torch.equal(torch.nan_to_num(a.geometry_data, nan=5.0), torch.nan_to_num(b.geometry_data, nan=5.0))
+        assert torch.equal(torch.nan_to_num(a.coefficient_data, nan=5.0),
+                           torch.nan_to_num(b.coefficient_data, nan=5.0))
