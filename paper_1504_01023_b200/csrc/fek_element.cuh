@@ -473,6 +473,118 @@ struct RegLoad {
   }
 };
 
+// ---------------------------------------------------------------------------
+// fp32 prism ConvDiff (QSS) on packed pairs (FFMA2 / FMUL2, sm_100).  The fp32
+// kernel is issue-bound, and Blackwell issues two fp32 FMAs per FFMA2.  Rows a
+// and a+3 (triangle function a on the two zeta levels) have reference
+// derivatives with the same zero pattern, so their gradients, A rows and b
+// entries run as one pair.  Each lane performs exactly the scalar path's
+// operations in the same order: results are bit-identical to it.
+// ---------------------------------------------------------------------------
+
+// g2[a][i] = (g[a][i], g[a+3][i]); Lin's rounding per lane (a +-1 coefficient
+// gives an exact product, so fma(c, x, acc) == acc + c*x there)
+template <int Q>
+__device__ __forceinline__ void prism_grads_x2(const Jac<float> &jac, float2 (&g2)[3][3]) {
+  using S = Shape<PRISM>;
+  static_for<3>([&](auto ac) {
+    FEK_CI(a, ac);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      float2 acc = make_float2(0.f, 0.f);
+      bool any = false;
+      static_for<3>([&](auto kc) {
+        FEK_CI(k, kc);
+        constexpr double c0 = S::ld(Q, a, k), c1 = S::ld(Q, a + 3, k);
+        static_assert((c0 == 0.0) == (c1 == 0.0), "paired rows share the zero pattern");
+        if constexpr (c0 != 0.0) {
+          const float2 c = make_float2(float(c0), float(c1));
+          const float x = jac.inv[k][i];
+          acc = any ? __ffma2_rn(c, make_float2(x, x), acc) : __fmul2_rn(c, make_float2(x, x));
+          any = true;
+        }
+      });
+      g2[a][i] = acc;
+    }
+  });
+}
+
+template <class Geo, class Load>
+__device__ __forceinline__ void integrate_prism_cd_x2(const Geo &geo, const float *coef, const Load &load, float tol,
+                                                      float (&A)[36], float (&B)[6], unsigned &fail_mask,
+                                                      unsigned &degen_mask) {
+  using S = Shape<PRISM>;
+  // pairs over the columns (a, a+3): A2[r][a] = (A[r][a], A[r][a+3]); the
+  // scalar operand of every FFMA2 (a C entry, a row's phi component) is a
+  // broadcast, so no pair is ever assembled from scalars
+  float2 A2[6][3], B2[3];  // B2[a] = (B[a], B[a+3])
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    B2[a] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < 6; ++r) A2[r][a] = make_float2(0.f, 0.f);
+  }
+  for_each_point<float, PRISM>(geo, tol, [&](auto qc, const auto &pd) {
+    FEK_CI(Q, qc);
+    fail_mask |= static_cast<unsigned>(pd.kind != 0) << Q;
+    degen_mask |= static_cast<unsigned>(pd.kind == KIND_DEGENERATE) << Q;
+    float2 g2[3][3];
+    prism_grads_x2<Q>(pd.jac, g2);
+    static_for<3>([&](auto ac) {
+      FEK_CI(a, ac);
+      // (t_a, t_a+3) = vol * C (phi_a, phi_a+3), per lane as cphi
+      const float2 val2 = make_float2(float(S::val(Q, a)), float(S::val(Q, a + 3)));
+      float2 t2[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float2 x = __fmul2_rn(val2, make_float2(coef[4 * i], coef[4 * i]));
+        x = __ffma2_rn(g2[a][2], make_float2(coef[4 * i + 3], coef[4 * i + 3]), x);
+        x = __ffma2_rn(g2[a][1], make_float2(coef[4 * i + 2], coef[4 * i + 2]), x);
+        x = __ffma2_rn(g2[a][0], make_float2(coef[4 * i + 1], coef[4 * i + 1]), x);
+        t2[i] = __fmul2_rn(x, make_float2(pd.vol, pd.vol));
+      }
+      // A[r][s] = acc_dot4(A[r][s], val_r, g_r, t_s) for s = a, a+3
+      static_for<6>([&](auto rc) {
+        FEK_CI(r, rc);
+        constexpr int ar = r % 3;
+        const float vr = float(S::val(Q, r));
+        const float g0 = r < 3 ? g2[ar][0].x : g2[ar][0].y;
+        const float g1 = r < 3 ? g2[ar][1].x : g2[ar][1].y;
+        const float gz = r < 3 ? g2[ar][2].x : g2[ar][2].y;
+        float2 acc = A2[r][a];
+        acc = __ffma2_rn(t2[0], make_float2(vr, vr), acc);
+        acc = __ffma2_rn(t2[1], make_float2(g0, g0), acc);
+        acc = __ffma2_rn(t2[2], make_float2(g1, g1), acc);
+        acc = __ffma2_rn(t2[3], make_float2(gz, gz), acc);
+        A2[r][a] = acc;
+      });
+    });
+    float tb[4];
+    load.fetch(tb);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tb[k] = pd.vol * tb[k];
+    static_for<3>([&](auto ac) {
+      FEK_CI(a, ac);
+      float2 acc = B2[a];
+      acc = __ffma2_rn(make_float2(float(S::val(Q, a)), float(S::val(Q, a + 3))), make_float2(tb[0], tb[0]), acc);
+      acc = __ffma2_rn(g2[a][0], make_float2(tb[1], tb[1]), acc);
+      acc = __ffma2_rn(g2[a][1], make_float2(tb[2], tb[2]), acc);
+      acc = __ffma2_rn(g2[a][2], make_float2(tb[3], tb[3]), acc);
+      B2[a] = acc;
+    });
+  });
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    B[a] = B2[a].x;
+    B[a + 3] = B2[a].y;
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      A[6 * r + a] = A2[r][a].x;
+      A[6 * r + a + 3] = A2[r][a].y;
+    }
+  }
+}
+
 template <typename R, int ET, int PB, int VAR, class Geo, class Load>
 __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef, const Load &load, R tol,
                                                   R (&A)[Shape<ET>::NS * Shape<ET>::NS],
@@ -493,7 +605,9 @@ __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef,
 #pragma unroll
   for (int i = 0; i < NS; ++i) B[i] = R(0);
 
-  if constexpr (VAR == QSS) {
+  if constexpr (VAR == QSS && sizeof(R) == 4 && ET == PRISM && !SYM) {
+    integrate_prism_cd_x2(geo, coef, load, tol, A, B, fail_mask, degen_mask);
+  } else if constexpr (VAR == QSS) {
     for_each_point<R, ET>(geo, tol, [&](auto qc, const auto &pd) {
       FEK_CI(Q, qc);
       note(pd.kind, Q);

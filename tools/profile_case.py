@@ -55,7 +55,13 @@ def main():
         torch.cuda.synchronize()
         times.append(s.elapsed_time(e))
     assert launch.error_key() == 0xFFFFFFFFFFFFFFFF
-    print(f"{args.case} {desc.short_name()} {args.dtype} n={launch.n} ms/launch={['%.4f' % t for t in times]}")
+    # bit-pattern digest of the outputs: equal digests <=> bit-identical results across builds
+    ia = launch.A.contiguous().view(-1).view(torch.int32 if dt == torch.float32 else torch.int64).to(torch.int64)
+    ib = launch.b.contiguous().view(-1).view(torch.int32 if dt == torch.float32 else torch.int64).to(torch.int64)
+    w = torch.arange(1, ia.numel() + 1, device="cuda", dtype=torch.int64)
+    digest = int((ia * w).sum().item()) ^ int((ib * w[: ib.numel()]).sum().item())
+    print(f"{args.case} {desc.short_name()} {args.dtype} n={launch.n} ms/launch={['%.4f' % t for t in times]} "
+          f"digest={digest & 0xFFFFFFFFFFFFFFFF:016x}")
 
 
 if __name__ == "__main__":
