@@ -81,12 +81,14 @@ def main():
     with open(args.out, "w") as fh:
         json.dump(data, fh, indent=1)
     if args.md:
-        lines = ["| kernel tag | us | DRAM R+W (MB) | DRAM % peak | FP64 pipe % | warps active % | regs | top stalls |",
-                 "|---|---|---|---|---|---|---|---|"]
+        lines = ["| kernel tag | us | DRAM R+W (MB) | DRAM % peak | FP64 pipe % | FMA pipe % | warps active % | regs | "
+                 "top stalls |",
+                 "|---|---|---|---|---|---|---|---|---|"]
         for tag, r in data.items():
             st = ", ".join(f"{k} {v}%" for k, v in list(r["stall_pct"].items())[:4])
             lines.append(f"| {tag} | {r.get('duration_us', 0):.1f} | {r['dram_bytes_per_launch'] / 1e6:.1f} | "
                          f"{r.get('dram_pct_peak', 0):.1f} | {r.get('fp64_pipe_pct', 0):.1f} | "
+                         f"{r.get('fma_pipe_pct', 0):.1f} | "
                          f"{r.get('warps_active_pct', 0):.1f} | {r.get('registers', 0):.0f} | {st} |")
         open(args.md, "w").write("\n".join(lines) + "\n")
     print(json.dumps(data, indent=1)[:3000])
