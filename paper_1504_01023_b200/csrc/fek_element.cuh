@@ -249,12 +249,45 @@ __device__ __forceinline__ void global_grad(const Jac<R> &jac, R (&g)[3]) {
   }
 }
 
+// Prism gradients from the factorisation of the reference derivatives
+// (refelem.py:145-155): ld[a] = (dlam_a * lo, -lam_a/2), ld[a+3] = (dlam_a * hi,
+// +lam_a/2) with dlam = (-1,-1), (1,0), (0,1).  With m_a = (lam_a/2) inv[2]:
+// g_a = lo (dlam_a . inv[0:2]) - m_a and g_a+3 = hi (dlam_a . inv[0:2]) + m_a --
+// 30 FP64 operations per point instead of 42.
+template <int Q, typename R>
+__device__ __forceinline__ void prism_grads(const Jac<R> &jac, R (&g)[6][3]) {
+  using S = Shape<PRISM>;
+  constexpr double lo = S::ld(Q, 1, 0), hi = S::ld(Q, 4, 0);
+  static_assert(S::ld(Q, 0, 0) == -lo && S::ld(Q, 0, 1) == -lo && S::ld(Q, 1, 1) == 0.0 && S::ld(Q, 2, 0) == 0.0 &&
+                S::ld(Q, 2, 1) == lo, "bottom-face derivative structure");
+  static_assert(S::ld(Q, 3, 0) == -hi && S::ld(Q, 3, 1) == -hi && S::ld(Q, 4, 1) == 0.0 && S::ld(Q, 5, 0) == 0.0 &&
+                S::ld(Q, 5, 1) == hi, "top-face derivative structure");
+  static_assert(S::ld(Q, 0, 2) == -S::ld(Q, 3, 2) && S::ld(Q, 1, 2) == -S::ld(Q, 4, 2) &&
+                S::ld(Q, 2, 2) == -S::ld(Q, 5, 2), "zeta derivative structure");
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const R x0 = jac.inv[0][i], x1 = jac.inv[1][i], x2 = jac.inv[2][i];
+    const R s01 = x0 + x1;
+    const R m0 = R(S::ld(Q, 3, 2)) * x2, m1 = R(S::ld(Q, 4, 2)) * x2, m2 = R(S::ld(Q, 5, 2)) * x2;
+    g[0][i] = fma(R(-lo), s01, -m0);
+    g[3][i] = fma(R(-hi), s01, m0);
+    g[1][i] = fma(R(lo), x0, -m1);
+    g[4][i] = fma(R(hi), x0, m1);
+    g[2][i] = fma(R(lo), x1, -m2);
+    g[5][i] = fma(R(hi), x1, m2);
+  }
+}
+
 template <int ET, int Q, typename R>
 __device__ __forceinline__ void all_grads(const Jac<R> &jac, R (&g)[Shape<ET>::NS][3]) {
-  static_for<Shape<ET>::NS>([&](auto sc) {
-    FEK_CI(s, sc);
-    global_grad<ET, Q, s>(jac, g[s]);
-  });
+  if constexpr (ET == PRISM && sizeof(R) == 8) {
+    prism_grads<Q>(jac, g);  // (fp32 pairs rows a, a+3 instead: prism_grads_x2)
+  } else {
+    static_for<Shape<ET>::NS>([&](auto sc) {
+      FEK_CI(s, sc);
+      global_grad<ET, Q, s>(jac, g[s]);
+    });
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -1,4 +1,4 @@
-for rep in 1 2; do for v in base er2; do
+for rep in 1 2; do for v in base pg; do
   for c in C4 C3; do FEK_LIB_OVERRIDE=tools/exp/libfek_$v.so timeout 300 python tools/profile_case.py --case $c --launches 8 2>&1 | sed "s/^/$v /" | tail -1; done
   FEK_LIB_OVERRIDE=tools/exp/libfek_$v.so timeout 300 python tools/profile_case.py --case C4 --dtype f32 --launches 8 2>&1 | sed "s/^/$v /" | tail -1
 done; done
