@@ -339,9 +339,10 @@ def _tile_queue(dev, stream: int):
     import torch
 
     key = (dev.index, stream)
-    q = _QUEUES.get(key)
-    if q is None:
-        q = _QUEUES[key] = torch.zeros(2, dtype=torch.int64, device=dev)
+    with _stream_lock:
+        q = _QUEUES.get(key)
+        if q is None:
+            q = _QUEUES[key] = torch.zeros(2, dtype=torch.int64, device=dev)
     return q
 
 
