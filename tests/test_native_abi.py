@@ -72,6 +72,27 @@ def test_descriptor_validation_without_gpu():
     assert lib.fek_host_workspace_bytes(ctypes.byref(d), 3, 1024) > 3 * 1024 * (18 + 6 + 36 + 6) * 8
 
 
+def test_v3_fields_validated_without_gpu():
+    """ABI v3: misaligned tile-queue words and bad layout-conversion arguments are refused up front."""
+    lib = _native.load()
+    d = _native.BatchDesc()
+    d.element, d.problem, d.variant, d.geometry_path = 0, 1, 0, 0
+    d.layout, d.lane_width, d.n_elements = 0, 1, 10
+    d.geometry = d.coefficients = d.stiffness = d.load = d.error_key = 256
+    d.scheduler = 260  # not 8-byte aligned
+    assert lib.fek_integrate(ctypes.byref(d), None) == _native.ERR_ALIGNMENT
+    d.ctas_per_sm = -1
+    assert lib.fek_integrate(ctypes.byref(d), None) == _native.ERR_ARGUMENT
+    # fek_convert_layout: lane widths, row size, dtype, aliasing
+    cv = lib.fek_convert_layout
+    assert cv(256, 3, 512, 1, 10, 12, 0, 0.0, None) == _native.ERR_ARGUMENT
+    assert cv(256, 1, 512, 128, 10, 12, 0, 0.0, None) == _native.ERR_ARGUMENT
+    assert cv(256, 1, 512, 4, 10, 43, 0, 0.0, None) == _native.ERR_ARGUMENT
+    assert cv(256, 1, 512, 4, 10, 12, 2, 0.0, None) == _native.ERR_ARGUMENT
+    assert cv(256, 1, 256, 4, 10, 12, 0, 0.0, None) == _native.ERR_ARGUMENT
+    assert cv(0, 1, 0, 4, 0, 12, 0, 0.0, None) == _native.OK  # empty: nothing to do
+
+
 def test_refconst_header_is_current():
     path = os.path.join(ROOT, "paper_1504_01023_b200", "csrc", "refconst.h")
     assert open(path).read() == gen_refconst.render()
