@@ -373,10 +373,20 @@ def _integrate_device(desc: KernelDescriptor, batch: DeviceBatch, out_layout, ch
                       out_layout=olayout if packed else None)
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream().cuda_stream
-        dd.scheduler = _tile_queue(dev, stream).data_ptr()
+        if torch.cuda.is_current_stream_capturing():
+            # CUDA-graph capture: a queue of the graph's own (zeroed on every
+            # replay by the captured fill), kept alive by the result
+            queue = torch.zeros(2, dtype=torch.int64, device=dev)
+            if check:
+                raise RuntimeError("integrate_batch inside CUDA-graph capture needs check=False "
+                                   "(read result.error_word after replay)")
+        else:
+            queue = _tile_queue(dev, stream)
+        dd.scheduler = queue.data_ptr()
         _native.check(lib.fek_integrate(ctypes.byref(dd), stream), "fek_integrate")
         result = BatchResult(desc, n, A, b, _traffic(desc, n), olayout, flat)
         result.error_word = err
+        result._queue = queue
         if check:
             key = int(err.item()) & _native.NO_ERROR
             if key != _native.NO_ERROR:
