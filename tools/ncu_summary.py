@@ -62,7 +62,37 @@ def read(rep):
     tot = sum(stalls.values()) or 1.0
     rec["stall_pct"] = {k: round(100 * v / tot, 1) for k, v in sorted(stalls.items(), key=lambda kv: -kv[1])[:8]}
     rec["dram_bytes_per_launch"] = rec.get("dram_read_bytes", 0) + rec.get("dram_write_bytes", 0)
+    rec.update(executed_flops(rep))
     return rec
+
+
+def executed_flops(rep):
+    """Executed FP64/FP32 flops per launch from the SASS source page (FMA counted as 2, FFMA2 as 4)."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = next((r for r in rows if "Source" in r and "Thread Instructions Executed" in r), None)
+    if hdr is None:
+        return {}
+    isrc, ithr = hdr.index("Source"), hdr.index("Thread Instructions Executed")
+    weights = {"DFMA": ("fp64", 2), "DMUL": ("fp64", 1), "DADD": ("fp64", 1),
+               "FFMA2": ("fp32", 4), "FMUL2": ("fp32", 2), "FADD2": ("fp32", 2),
+               "FFMA": ("fp32", 2), "FMUL": ("fp32", 1), "FADD": ("fp32", 1)}
+    tot = {"fp64": 0.0, "fp32": 0.0}
+    for r in rows[rows.index(hdr) + 1:]:
+        if len(r) <= max(isrc, ithr):
+            continue
+        words = r[isrc].split()
+        if not words:
+            continue
+        op = (words[1] if words[0].startswith("@") and len(words) > 1 else words[0]).split(".")[0]
+        if op in weights:
+            kind, w = weights[op]
+            try:
+                tot[kind] += w * float(r[ithr].replace(",", ""))
+            except ValueError:
+                pass
+    return {"executed_fp64_flops": tot["fp64"], "executed_fp32_flops": tot["fp32"]}
 
 
 def main():
@@ -81,14 +111,15 @@ def main():
     with open(args.out, "w") as fh:
         json.dump(data, fh, indent=1)
     if args.md:
-        lines = ["| kernel tag | us | DRAM R+W (MB) | DRAM % peak | FP64 pipe % | FMA pipe % | warps active % | regs | "
-                 "top stalls |",
-                 "|---|---|---|---|---|---|---|---|---|"]
+        lines = ["| kernel tag | us | DRAM R+W (MB) | DRAM % peak | FP64 pipe % | FMA pipe % | executed TFLOP/s "
+                 "(FMA = 2) | warps active % | regs | top stalls |",
+                 "|---|---|---|---|---|---|---|---|---|---|"]
         for tag, r in data.items():
             st = ", ".join(f"{k} {v}%" for k, v in list(r["stall_pct"].items())[:4])
             lines.append(f"| {tag} | {r.get('duration_us', 0):.1f} | {r['dram_bytes_per_launch'] / 1e6:.1f} | "
                          f"{r.get('dram_pct_peak', 0):.1f} | {r.get('fp64_pipe_pct', 0):.1f} | "
                          f"{r.get('fma_pipe_pct', 0):.1f} | "
+                         f"{(r.get('executed_fp64_flops', 0) + r.get('executed_fp32_flops', 0)) / (r.get('duration_us', 1) * 1e6):.1f} | "
                          f"{r.get('warps_active_pct', 0):.1f} | {r.get('registers', 0):.0f} | {st} |")
         open(args.md, "w").write("\n".join(lines) + "\n")
     print(json.dumps(data, indent=1)[:3000])
