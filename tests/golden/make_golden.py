@@ -216,11 +216,55 @@ def unit_elements():
     _save("unit_elements.npz", **out)
 
 
+SLICE = 1024  # sampled elements per benchmark configuration
+
+
+def bench_slices(keys=("C1", "C2", "C3", "C4", "C5T", "C5P")):
+    """The benchmark configurations end to end through the reference.
+
+    The full mesh comes from the reference's own generate_mesh (coefficient
+    seed as in the benchmark).  Prism configurations add the benchmark's
+    top-face jitter, restated by paper_1504_01023_b200.mesh.jitter_top_faces,
+    since the reference applies it only in its verification corpus
+    (verify.py:85-86).  1024 sampled elements are then integrated by the
+    reference's integrate_batch with the natural QSS descriptor: the first
+    and last 128 elements plus 768 seeded random ones.  The GPU test
+    regenerates each configuration with the device mesh generator, checks the
+    sampled inputs bit for bit, and compares its outputs with the
+    reference's.
+    """
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_1504_01023_b200 import mesh as M  # host restatement: specs and jitter only
+
+    for key in keys:
+        cfg = M.bench_configs()[key]
+        spec = MeshSpec(cfg.spec.nx, cfg.spec.ny, cfg.spec.nz, ElementType(cfg.spec.element_type.value))
+        problem = ProblemClass(cfg.problem.value)
+        batch = generate_mesh(spec, cfg.coeff_seed, problem)
+        geo, cof = batch.geometry_rows(), batch.coefficient_rows()
+        if cfg.jitter_seed is not None:
+            geo = M.jitter_top_faces(geo, cfg.spec, cfg.jitter_seed)
+        n = geo.shape[0]
+        rng = np.random.default_rng(SEED + 7)
+        idx = np.unique(np.concatenate([np.arange(128), np.arange(n - 128, n),
+                                        rng.choice(n, SLICE - 256, replace=False)]))
+        g, c = np.ascontiguousarray(geo[idx]), np.ascontiguousarray(cof[idx])
+        desc = case_descriptors(spec.element_type, problem)[0]
+        res = integrate_batch(desc, ElementBatch.from_arrays(spec.element_type, problem, g, c))
+        _save(f"bench_{key}.npz", index=idx, geometry_rows=g, coefficient_rows=c, A=res.stiffness, b=res.load,
+              n_elements=np.array([n]))
+        del batch, geo, cof
+
+
 if __name__ == "__main__":
     print("reference feklab", feklab.__version__, "from", os.path.dirname(feklab.__file__), file=sys.stderr)
+    if sys.argv[1:] == ["bench"]:
+        bench_slices()
+        sys.exit(0)
     refelem()
     corpora()
     twisted_prisms()
     meshes()
     error_cases()
     unit_elements()
+    bench_slices()

@@ -162,3 +162,14 @@ def test_duck_typed_descriptor_coercion():
     with pytest.raises(TypeError):
         coerce_descriptor(SimpleNamespace(variant=e("xyz"), geometry_path=e("generic"), problem=e("poisson"),
                                           element=e("prism")))
+
+
+@pytest.mark.parametrize("key", ["C1", "C2", "C3"])
+def test_bench_inputs_equal_reference_generator(key):
+    """Host restatement of the benchmark inputs == the reference's generate_mesh (sampled, full size)."""
+    z = golden(f"bench_{key}.npz")
+    cfg = mesh.bench_configs()[key]
+    geo, cof = mesh.config_rows(cfg)
+    assert geo.shape[0] == int(z["n_elements"][0])
+    assert np.array_equal(geo[z["index"]], z["geometry_rows"])
+    assert np.array_equal(cof[z["index"]], z["coefficient_rows"])
