@@ -108,6 +108,9 @@ typedef struct fek_batch_desc {
 } fek_batch_desc;
 
 int fek_abi_version(void);
+/* sizeof(fek_batch_desc) as compiled: a binding checks its own struct
+ * layout against this before the first call */
+size_t fek_batch_desc_size(void);
 const char *fek_status_string(int status);
 /* message of the last CUDA error seen by this thread (empty if none) */
 const char *fek_last_cuda_error(void);

@@ -63,6 +63,7 @@ _P = ctypes.c_void_p
 _DP = ctypes.POINTER(BatchDesc)
 SIGNATURES = {
     "fek_abi_version": (ctypes.c_int, []),
+    "fek_batch_desc_size": (ctypes.c_size_t, []),
     "fek_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "fek_last_cuda_error": (ctypes.c_char_p, []),
     "fek_integrate": (ctypes.c_int, [_DP, _P]),
@@ -110,6 +111,9 @@ def load() -> ctypes.CDLL:
             fn.restype, fn.argtypes = res, args
         if lib.fek_abi_version() != ABI_VERSION:
             raise NativeLibraryError(f"libfek ABI {lib.fek_abi_version()} != expected {ABI_VERSION}")
+        if lib.fek_batch_desc_size() != ctypes.sizeof(BatchDesc):
+            raise NativeLibraryError(f"fek_batch_desc is {lib.fek_batch_desc_size()} bytes in libfek, "
+                                     f"{ctypes.sizeof(BatchDesc)} in the ctypes binding")
         _lib = lib
     return _lib
 

@@ -230,6 +230,8 @@ extern "C" {
 
 int fek_abi_version(void) { return FEK_ABI_VERSION; }
 
+size_t fek_batch_desc_size(void) { return sizeof(fek_batch_desc); }
+
 const char *fek_status_string(int status) {
   switch (status) {
     case FEK_OK: return "ok";

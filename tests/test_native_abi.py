@@ -112,3 +112,17 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setattr(_native, "LIB_PATH", str(tmp_path / "nope.so"))
     with pytest.raises(_native.NativeLibraryError):
         _native.load()
+
+
+def test_integration_stub_struct_matches_the_library():
+    """The ctypes stub in INTEGRATION.md lays out fek_batch_desc exactly as libfek does."""
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    start = text.index("class _Desc(ctypes.Structure)")
+    block = text[start:text.index("\n\n", start)]
+    ns = {"ctypes": ctypes}
+    exec(block, ns)
+    stub = ns["_Desc"]
+    lib = _native.load()
+    assert ctypes.sizeof(stub) == lib.fek_batch_desc_size() == ctypes.sizeof(_native.BatchDesc)
+    ours = {name: getattr(_native.BatchDesc, name).offset for name, _ in _native.BatchDesc._fields_}
+    assert {name: getattr(stub, name).offset for name, _ in stub._fields_} == ours
