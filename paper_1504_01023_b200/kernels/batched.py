@@ -244,6 +244,54 @@ class DeviceBatch:
         return ElementBatch(self.element_type, self.problem, self.n_elements, self.layout, geo, cof)
 
 
+def _read_device_batch(path, device, dtype=None, chunk_bytes: int = 64 << 20) -> DeviceBatch:
+    """FEKB file -> DeviceBatch through two alternating page-locked staging buffers."""
+    import torch
+
+    from ..layout import _read_header
+
+    device = torch.device(device)
+    if device.index is None:
+        device = torch.device(device.type, torch.cuda.current_device())
+    dtype = dtype or torch.float64
+    chunk = max(1, chunk_bytes // 8)
+    with open(path, "rb") as fh, torch.cuda.device(device):
+        etype, problem, layout, n = _read_header(fh, path)
+        stream = torch.cuda.Stream(device)
+        staging = [torch.empty(chunk, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+        scratch = torch.empty(chunk, dtype=torch.float64, device=device) if dtype != torch.float64 else None
+        done = [None, None]
+        out = []
+        k = 0
+        for ds in (etype.geometry_size, problem.coefficient_size(etype)):
+            size = flat_length(n, ds, layout)
+            dst = torch.empty(size, dtype=dtype, device=device)
+            for lo in range(0, size, chunk):
+                cnt = min(chunk, size - lo)
+                slot = k % 2
+                if done[slot] is not None:
+                    done[slot].synchronize()  # the upload that last used this buffer has finished
+                buf = staging[slot][:cnt]
+                got = fh.readinto(memoryview(buf.numpy()).cast("B"))
+                if got != cnt * 8:
+                    raise ValueError(f"{path}: truncated data section")
+                with torch.cuda.stream(stream):
+                    if scratch is None:
+                        dst[lo:lo + cnt].copy_(buf, non_blocking=True)
+                    else:
+                        scratch[:cnt].copy_(buf, non_blocking=True)
+                        dst[lo:lo + cnt].copy_(scratch[:cnt])
+                    done[slot] = torch.cuda.Event()
+                    done[slot].record(stream)
+                k += 1
+            out.append(dst)
+        if fh.read(1):
+            raise ValueError(f"{path}: trailing bytes after data section")
+        torch.cuda.current_stream(device).wait_stream(stream)
+        stream.synchronize()
+    return DeviceBatch(etype, problem, int(n), layout, out[0], out[1])
+
+
 # ---------------------------------------------------------------------------
 # descriptor plumbing
 # ---------------------------------------------------------------------------

@@ -105,3 +105,26 @@ def test_convert_unaligned_arrays_take_the_plain_kernel():
         assert torch.equal(torch.nan_to_num(a.geometry_data, nan=5.0), torch.nan_to_num(b.geometry_data, nan=5.0))
         assert torch.equal(torch.nan_to_num(a.coefficient_data, nan=5.0),
                            torch.nan_to_num(b.coefficient_data, nan=5.0))
+
+
+@pytest.mark.parametrize("w", [1, 8])
+def test_fekb_streams_into_device_batch(tmp_path, w):
+    """read_batch(path, device=...) streams a FEKB file through pinned staging into HBM."""
+    import torch
+
+    from paper_1504_01023_b200 import read_batch, write_batch
+    from paper_1504_01023_b200.kernels.batched import _read_device_batch
+
+    hb = host_batch(ElementType.PRISM, ProblemClass.CONV_DIFF, 20_011, w)
+    path = tmp_path / "mesh.fekb"
+    write_batch(hb, path)
+    for db in (read_batch(path, device="cuda"), _read_device_batch(path, "cuda", chunk_bytes=4096 * 8 + 8)):
+        assert isinstance(db, DeviceBatch) and db.layout == hb.layout and db.n_elements == hb.n_elements
+        assert np.array_equal(db.geometry_data.cpu().numpy(), hb.geometry_data, equal_nan=True)
+        assert np.array_equal(db.coefficient_data.cpu().numpy(), hb.coefficient_data, equal_nan=True)
+    d32 = _read_device_batch(path, "cuda", dtype=torch.float32, chunk_bytes=1 << 16)
+    assert d32.dtype == torch.float32
+    assert np.array_equal(d32.geometry_data.cpu().numpy(), hb.geometry_data.astype(np.float32), equal_nan=True)
+    desc = case_descriptors(ElementType.PRISM, ProblemClass.CONV_DIFF)[0]
+    r1, r2 = integrate_batch(desc, read_batch(path, device="cuda")), integrate_batch(desc, read_batch(path))
+    assert np.array_equal(r1.stiffness.cpu().numpy(), r2.stiffness)
