@@ -5,20 +5,20 @@ TEST / BASELINE INFRASTRUCTURE ONLY (see numpy_oracle.py).  Used by
 
 The reference itself is a numpy program whose ``workers`` threads contend for
 the GIL (its own measurements: workers=1 is fastest).  To give
-the CPU arm "all the host threads it can use", this runner forks one process
+the CPU arm "all the host threads it can use", this runner starts one process
 per core, each running the bitwise-faithful numpy restatement
 (``numpy_oracle.integrate``) on a contiguous element range -- the reference's
-own worker split (``batched.py:573``) -- writing into shared anonymous
-memory.  ``kind`` is therefore "port": the reference's algorithm and numpy
-arithmetic, parallelised across processes instead of GIL-bound threads.
+own worker split (``batched.py:573``) -- writing into named shared memory.
+``kind`` is therefore "port": the reference's algorithm and numpy arithmetic,
+parallelised across processes instead of GIL-bound threads.
 """
 
 from __future__ import annotations
 
-import mmap
 import multiprocessing as mp
 import os
 import time
+from multiprocessing import shared_memory
 
 import numpy as np
 
@@ -27,12 +27,46 @@ from . import numpy_oracle as O
 _STATE = {}
 
 
-def _shared(shape) -> np.ndarray:
-    size = int(np.prod(shape)) * 8
-    buf = mmap.mmap(-1, max(size, 8))
-    arr = np.frombuffer(buf, dtype=np.float64, count=int(np.prod(shape))).reshape(shape)
-    arr.fill(0.0)  # fault the pages in before forking, so timed runs measure compute only
-    return arr
+class _Shared:
+    """A named shared-memory float64 array (the workers attach by name)."""
+
+    def __init__(self, shape, fill=None):
+        self.shape = tuple(int(x) for x in shape)
+        size = max(int(np.prod(self.shape)) * 8, 8)
+        self.shm = shared_memory.SharedMemory(create=True, size=size)
+        self.array = np.ndarray(self.shape, dtype=np.float64, buffer=self.shm.buf)
+        if fill is None:
+            self.array.fill(0.0)  # fault the pages in before timing
+        else:
+            self.array[...] = fill
+
+    def spec(self):
+        return self.shm.name, self.shape
+
+    def close(self):
+        self.array = None
+        try:
+            self.shm.close()
+        except BufferError:  # a caller still holds a view; the mapping goes with it
+            pass
+        self.shm.unlink()
+
+
+def _attach(name, shape):
+    # (forkserver workers share the parent's resource tracker, which the
+    # parent's unlink() settles; attaching re-registers the same name)
+    shm = shared_memory.SharedMemory(name=name)
+    return shm, np.ndarray(shape, dtype=np.float64, buffer=shm.buf)
+
+
+def _init_worker(config, specs):
+    _STATE.clear()
+    _STATE.update(config)
+    _STATE["_shm"] = []
+    for key, (name, shape) in specs.items():
+        shm, arr = _attach(name, shape)
+        _STATE["_shm"].append(shm)
+        _STATE[key] = arr
 
 
 def _work(args):
@@ -47,18 +81,28 @@ def _work(args):
 
 
 class PortPool:
-    """Fork pool holding one workload; ``run(lo, hi)`` integrates a range in parallel."""
+    """Process pool holding one workload; ``run(lo, hi)`` integrates a range in parallel.
+
+    Workers come from a ``forkserver`` (a clean single-threaded parent), not
+    a fork of this process -- which may hold CUDA and torch threads -- and
+    see the inputs and outputs through named shared memory.
+    """
 
     def __init__(self, variant, path, problem, etype, geo_rows, coef_rows, processes: int | None = None):
         self.processes = processes or os.cpu_count() or 1
         ns = 4 if etype == O.TET else 6
         n = geo_rows.shape[0]
-        _STATE.clear()
-        _STATE.update(variant=variant, path=path, problem=problem, etype=etype,
-                      geo=np.ascontiguousarray(geo_rows), coef=np.ascontiguousarray(coef_rows),
-                      A=_shared((n, ns, ns)), b=_shared((n, ns)))
-        self.A, self.b = _STATE["A"], _STATE["b"]
-        self._pool = mp.get_context("fork").Pool(self.processes) if self.processes > 1 else None
+        config = dict(variant=variant, path=path, problem=problem, etype=etype)
+        self._arrays = {"geo": _Shared(geo_rows.shape, geo_rows), "coef": _Shared(coef_rows.shape, coef_rows),
+                        "A": _Shared((n, ns, ns)), "b": _Shared((n, ns))}
+        self.A, self.b = self._arrays["A"].array, self._arrays["b"].array
+        specs = {k: v.spec() for k, v in self._arrays.items()}
+        if self.processes > 1:
+            self._pool = mp.get_context("forkserver").Pool(self.processes, initializer=_init_worker,
+                                                           initargs=(config, specs))
+        else:
+            self._pool = None
+            _init_worker(config, specs)
 
     def run(self, lo: int, hi: int) -> float:
         """Integrate elements [lo, hi); returns wall seconds."""
@@ -78,6 +122,13 @@ class PortPool:
             self._pool.close()
             self._pool.join()
             self._pool = None
+        for shm in _STATE.pop("_shm", []):
+            shm.close()
+        _STATE.clear()
+        self.A = self.b = None
+        for arr in self._arrays.values():
+            arr.close()
+        self._arrays = {}
 
     def __enter__(self):
         return self
