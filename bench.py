@@ -2,7 +2,8 @@
 """bench.py -- elements integrated per second on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...           (N > 1)
+    torchrun --nproc-per-node N bench.py --gpus N ...           (N > 1; plain `python bench.py
+                                                                --gpus N` starts torchrun itself)
 
 Headline workload (N=1, BASELINE.json configs[1] -> SURVEY config C2):
 generalized convection-diffusion-reaction on 4,088,832 linear tetrahedra
@@ -633,8 +634,23 @@ def run_c5(args) -> int:
     return 0
 
 
+def _relaunch_under_torchrun(args, argv) -> int:
+    """`python bench.py --gpus N` (N > 1) without torchrun: start N ranks on this node."""
+    import socket
+    import subprocess
+
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)]
+    return subprocess.call(cmd + list(sys.argv[1:] if argv is None else argv))
+
+
 def main(argv=None) -> int:
     args = parse(argv)
+    if args.gpus > 1 and not launched_by_torchrun():
+        return _relaunch_under_torchrun(args, argv)
     if args.impl == "reference":
         return run_reference(args)
     if args.config == "C5":
