@@ -13,6 +13,8 @@ from .kernels import (BatchResult, DeviceBatch, TrafficCounters, access_breakdow
                       integrate_batch, integrate_element, launch_config, phase_op_counts)
 from .layout import (ELEMENT_MAJOR, LANE_WIDTHS, BatchLayout, ElementBatch, LayoutKind, build_batch, convert,
                      extract, flat_length, pack_rows, read_batch, unpack_rows, write_batch)
+from .perfmodel import (B200_NOMINAL, BUILTIN_PROFILES, KernelCost, ProcessorProfile, b200_profile, efficiency,
+                        kernel_cost, limiting_intensity, memory_requirements, time_bound)
 from .problems import (CoefficientSet, ElementMatrix, GeometryPath, KernelDescriptor, ProblemClass, Variant,
                        all_descriptors, case_descriptors, natural_path)
 from .refelem import ElementType, QuadratureRule, ShapeFunctionTable, reference_element, shape_at
@@ -20,6 +22,8 @@ from .refelem import ElementType, QuadratureRule, ShapeFunctionTable, reference_
 __version__ = "0.1.0"
 
 __all__ = [
+    "B200_NOMINAL", "BUILTIN_PROFILES", "KernelCost", "ProcessorProfile", "b200_profile", "efficiency",
+    "kernel_cost", "limiting_intensity", "memory_requirements", "time_bound",
     "BatchLayout", "BatchResult", "CoefficientSet", "CounterMismatch", "DEGENERACY_REL_TOL", "DegenerateElement",
     "DeviceBatch", "ELEMENT_MAJOR", "ElementBatch", "ElementGeometry", "ElementMatrix", "ElementType",
     "FeklabError", "GeometryError", "GeometryPath", "HeterogeneousBatch", "InvertedElement", "KernelDescriptor",

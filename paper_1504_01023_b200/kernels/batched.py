@@ -250,12 +250,17 @@ def _read_device_batch(path, device, dtype=None, chunk_bytes: int = 64 << 20) ->
 
     from ..layout import _read_header
 
-    device = torch.device(device)
-    if device.index is None:
-        device = torch.device(device.type, torch.cuda.current_device())
+    fh = open(path, "rb")  # an unreadable file fails as OSError before any CUDA call, as on the host path
+    try:
+        device = torch.device(device)
+        if device.index is None:
+            device = torch.device(device.type, torch.cuda.current_device())
+    except BaseException:
+        fh.close()
+        raise
     dtype = dtype or torch.float64
     chunk = max(1, chunk_bytes // 8)
-    with open(path, "rb") as fh, torch.cuda.device(device):
+    with fh, torch.cuda.device(device):
         etype, problem, layout, n = _read_header(fh, path)
         stream = torch.cuda.Stream(device)
         staging = [torch.empty(chunk, dtype=torch.float64, pin_memory=True) for _ in range(2)]

@@ -8,6 +8,10 @@ unchanged).  The reference sweeps storage layout x lane width x worker count
 on the CPU.  Here the sweep is layout x lane width x loop-order variant x
 geometry path on the GPU; the ``workers`` column holds the GPU count.
 
+This is the extended study (every loop-order variant and geometry path on
+device-generated benchmark meshes); ``python -m paper_1504_01023_b200 tune``
+is the reference CLI's single-descriptor layout/worker sweep.
+
 Inputs are generated in HBM by the device mesh generator (``mesh.device_config``)
 and re-laid-out on the device.  Each point is the median of ``repeats``
 CUDA-event-timed launches.  The model bound is the reference's
@@ -23,9 +27,7 @@ import io
 import statistics
 import sys
 
-CSV_COLUMNS = ("variant", "geo", "element", "problem", "layout", "lane_width", "workers", "n_elements",
-               "ns_per_element", "ns_mad", "accesses_per_element", "ops_model", "intensity", "bound_ns",
-               "efficiency_pct")
+from .bench import CSV_COLUMNS
 
 
 def b200_profile():
