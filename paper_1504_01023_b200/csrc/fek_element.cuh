@@ -593,10 +593,14 @@ __device__ __forceinline__ R xdot(const R &acc, R lam_a, R k0, R k1, R k2) {
 
 // distinct Jacobian columns (for_each_point's reuse): J2[t][i] = J[i][2] at triangle point t,
 // J01[z][i][k] = J[i][k] (k = 0, 1) on level z -- bitwise the reference's per-point J
-template <typename R, class Geo>
-__device__ __forceinline__ void jacobian_columns(const Geo &geo, R (&J2)[3][3], R (&J01)[2][3][2]) {
-  R X[18];
-  geo.fetch(X);
+template <typename R>
+struct Cols {
+  R J2[3][3];      // [t][i]
+  R J01[2][3][2];  // [z][i][k]
+};
+
+template <typename R>
+__device__ __forceinline__ void jacobian_columns(const R (&X)[18], R (&J2)[3][3], R (&J01)[2][3][2]) {
   static_for<3>([&](auto tc) {
     FEK_CI(t, tc);
 #pragma unroll
@@ -631,16 +635,16 @@ __device__ __forceinline__ R adjugate(const R (&J01)[3][2], const R (&J2)[3], R 
 }
 }  // namespace prism_ref
 
-template <typename R, class Geo, class Load>
-__device__ __forceinline__ void integrate_prism_cd_ref(const Geo &geo, const R *c, const Load &load, R tol,
+template <typename R, class Coef>
+__device__ __forceinline__ void integrate_prism_cd_ref(const prism_ref::Cols<R> &cols, const Coef &c, R tol,
                                                        R (&A)[36], R (&B)[6], unsigned &fail_mask,
                                                        unsigned &degen_mask) {
   using namespace prism_ref;
   constexpr double w = S::w(0);
-  R d[4];
-  load.fetch(d);
-  R J2[3][3], J01[2][3][2];
-  jacobian_columns(geo, J2, J01);
+  // coefficient row: c00 .. c33, d0 .. d3 (problems.py:136-140)
+  auto d = [&](int k) { return c[16 + k]; };
+  const auto &J2 = cols.J2;
+  const auto &J01 = cols.J01;
   // per-level sums [z]; SYY / SbY carry the same weight on both levels
   R SXX[2][3][3], SXY[2][3][3], SYX[2][3][3], SbX[2][3];
   R SYY[6], SbY[3];
@@ -706,10 +710,10 @@ __device__ __forceinline__ void integrate_prism_cd_ref(const Geo &geo, const R *
         });
       });
       // load: e = vol P^T d / w = (det d0, adj d[1:4])
-      const R e0 = det * d[0];
+      const R e0 = det * d(0);
       R e[3];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) e[k] = fma(adj[k][0], d[1], fma(adj[k][1], d[2], adj[k][2] * d[3]));
+      for (int k = 0; k < 3; ++k) e[k] = fma(adj[k][0], d(1), fma(adj[k][1], d(2), adj[k][2] * d(3)));
       static_for<3>([&](auto ac) {
         FEK_CI(a, ac);
         SbX[z][a] = xdot<a, F>(SbX[z][a], L[a], e0, e[0], e[1]);
@@ -762,13 +766,14 @@ __device__ __forceinline__ void integrate_prism_cd_ref(const Geo &geo, const R *
 //   YY[a][a'] = lam_a lam_a' K[zeta][zeta].
 // Load: b_(a,b) = w sum_z l_b(z) sum_t lam_a(t) det_q d0[q].
 // About 620 FP64 instructions per element instead of ~900.
-template <typename R, class Geo>
-__device__ __forceinline__ void integrate_prism_poisson_ref(const Geo &geo, const R *d0, R tol, R (&A)[36], R (&B)[6],
-                                                            unsigned &fail_mask, unsigned &degen_mask) {
+template <typename R>
+__device__ __forceinline__ void integrate_prism_poisson_ref(const prism_ref::Cols<R> &cols, const R *d0, R tol,
+                                                            R (&A)[36], R (&B)[6], unsigned &fail_mask,
+                                                            unsigned &degen_mask) {
   using namespace prism_ref;
   constexpr double w = S::w(0);
-  R J2[3][3], J01[2][3][2];
-  jacobian_columns(geo, J2, J01);
+  const auto &J2 = cols.J2;
+  const auto &J01 = cols.J01;
   R SK[2][3];      // sum_t (k00, k01, k11) of the (xi, eta) block, per level
   R SXY[2][2][3];  // [z][a-1][a'] = sum_t lam_a'(t) p_a, p_1 = k02, p_2 = k12 (p_0 = -p_1 - p_2)
   R SYY[6];        // sum_q lam_a lam_a' k22 (packed symmetric)
@@ -868,6 +873,25 @@ __device__ __forceinline__ void integrate_prism_poisson_ref(const Geo &geo, cons
   });
 }
 
+// QSS prism kernels from the element's distinct Jacobian columns (computed by
+// the caller, so the input stage can be released before the math starts)
+template <typename R, int PB, class Coef>
+__device__ __forceinline__ void integrate_prism_qss(const prism_ref::Cols<R> &cols, const Coef &coef, R tol,
+                                                    R (&A)[36], R (&B)[6], int &kind, int &kind_point) {
+  unsigned fail_mask = 0, degen_mask = 0;
+  if constexpr (PB == POISSON) {
+    integrate_prism_poisson_ref<R>(cols, coef, tol, A, B, fail_mask, degen_mask);
+  } else {
+    integrate_prism_cd_ref<R>(cols, coef, tol, A, B, fail_mask, degen_mask);
+  }
+  kind = 0;
+  kind_point = -1;
+  if (fail_mask) {  // the SMALLEST failing point, as in the reference
+    kind_point = __ffs(fail_mask) - 1;
+    kind = ((degen_mask >> kind_point) & 1u) ? KIND_DEGENERATE : KIND_INVERTED;
+  }
+}
+
 template <typename R, int ET, int PB, int VAR, class Geo, class Load>
 __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef, const Load &load, R tol,
                                                   R (&A)[Shape<ET>::NS * Shape<ET>::NS],
@@ -888,10 +912,18 @@ __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef,
 #pragma unroll
   for (int i = 0; i < NS; ++i) B[i] = R(0);
 
-  if constexpr (VAR == QSS && ET == PRISM && !SYM) {
-    integrate_prism_cd_ref<R>(geo, coef, load, tol, A, B, fail_mask, degen_mask);
-  } else if constexpr (VAR == QSS && ET == PRISM && SYM && sizeof(R) == 8) {
-    integrate_prism_poisson_ref<R>(geo, coef, tol, A, B, fail_mask, degen_mask);
+  if constexpr (VAR == QSS && ET == PRISM && (!SYM || sizeof(R) == 8)) {
+    prism_ref::Cols<R> cols;
+    {
+      R X[DSG];
+      geo.fetch(X);
+      prism_ref::jacobian_columns(X, cols.J2, cols.J01);
+    }
+    if constexpr (SYM) {
+      integrate_prism_poisson_ref<R>(cols, coef, tol, A, B, fail_mask, degen_mask);
+    } else {
+      integrate_prism_cd_ref<R>(cols, coef, tol, A, B, fail_mask, degen_mask);
+    }
   } else if constexpr (VAR == QSS) {
     for_each_point<R, ET>(geo, tol, [&](auto qc, const auto &pd) {
       FEK_CI(Q, qc);
