@@ -26,6 +26,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "fek_device.cuh"
 #include "refconst.h"
@@ -564,7 +565,7 @@ static_assert(structure_ok(), "prism reference tables factor as lam_a(t) l_b(z)"
 // acc (+)= X_a . (k0, k1, k2) with X_a = (lam, dlam_a): one FMA plus the +-1 terms
 // s (+)= x * y; the first term of a sum is a plain product
 template <bool FIRST, typename R>
-__device__ __forceinline__ void mac(R &s, R x, R y) {
+__device__ __forceinline__ void mac(R &s, const R &x, const R &y) {
   if constexpr (FIRST) {
     s = x * y;
   } else {
@@ -573,7 +574,7 @@ __device__ __forceinline__ void mac(R &s, R x, R y) {
 }
 
 template <int A_, bool FIRST, typename R>
-__device__ __forceinline__ R xdot(const R &acc, R lam_a, R k0, R k1, R k2) {
+__device__ __forceinline__ R xdot(const R &acc, const R &lam_a, const R &k0, const R &k1, const R &k2) {
   R r;
   if constexpr (FIRST) {
     r = lam_a * k0;
@@ -618,6 +619,7 @@ __device__ __forceinline__ void jacobian_columns(const R (&X)[18], R (&J2)[3][3]
 // adjugate (adj[k][i] = det * d xi_k / d x_i) and determinant of J = [J01 | J2], invert3's operations
 template <typename R>
 __device__ __forceinline__ R adjugate(const R (&J01)[3][2], const R (&J2)[3], R (&adj)[3][3]) {
+  // (also instantiated for fp32 pairs, where -(x * y) is a packed negation)
   const R a_ = J01[0][0], b_ = J01[0][1], c_ = J2[0];
   const R d_ = J01[1][0], e_ = J01[1][1], f_ = J2[1];
   const R g_ = J01[2][0], h_ = J01[2][1], i_ = J2[2];
@@ -635,57 +637,127 @@ __device__ __forceinline__ R adjugate(const R (&J01)[3][2], const R (&J2)[3], R 
 }
 }  // namespace prism_ref
 
+// Two fp32 lanes on sm_100's packed FFMA2 / FMUL2 / FADD2: the fp32 prism
+// kernel runs both zeta levels of a triangle point as one pair (the per-point
+// work is identical on the two levels, with the same compile-time constants).
+struct f2 {
+  float2 v;
+  __device__ __forceinline__ f2() {}
+  __device__ __forceinline__ f2(float x) : v(make_float2(x, x)) {}
+  __device__ __forceinline__ f2(float x, float y) : v(make_float2(x, y)) {}
+  __device__ __forceinline__ explicit f2(float2 p) : v(p) {}
+};
+__device__ __forceinline__ f2 operator*(f2 a, f2 b) { return f2(__fmul2_rn(a.v, b.v)); }
+__device__ __forceinline__ f2 operator+(f2 a, f2 b) { return f2(__fadd2_rn(a.v, b.v)); }
+__device__ __forceinline__ f2 operator-(f2 a) { return f2(make_float2(-a.v.x, -a.v.y)); }
+__device__ __forceinline__ f2 operator-(f2 a, f2 b) { return f2(__ffma2_rn(b.v, make_float2(-1.f, -1.f), a.v)); }
+__device__ __forceinline__ f2 fma(f2 a, f2 b, f2 c) { return f2(__ffma2_rn(a.v, b.v, c.v)); }
+using ::fma;  // keep the scalar overloads visible next to the pair one
+
+namespace prism_ref {
+template <typename V>
+struct Lanes;  // per-level view of a value: scalar (one level) or pair (both levels)
+template <>
+struct Lanes<double> {
+  static constexpr int NZ = 2;  // levels looped
+  __device__ static double get(double x, int) { return x; }
+};
+template <>
+struct Lanes<float> {
+  static constexpr int NZ = 2;
+  __device__ static float get(float x, int) { return x; }
+};
+template <>
+struct Lanes<f2> {
+  static constexpr int NZ = 1;  // both levels in one pass
+  __device__ static float get(f2 x, int lane) { return lane ? x.v.y : x.v.x; }
+};
+
+__device__ __forceinline__ unsigned kind_bits(double det, double tol, int q, unsigned &degen) {
+  const int k = classify(det, tol);
+  degen |= static_cast<unsigned>(k == KIND_DEGENERATE) << q;
+  return static_cast<unsigned>(k != 0) << q;
+}
+__device__ __forceinline__ unsigned kind_bits(float det, float tol, int q, unsigned &degen) {
+  const int k = classify(det, tol);
+  degen |= static_cast<unsigned>(k == KIND_DEGENERATE) << q;
+  return static_cast<unsigned>(k != 0) << q;
+}
+// pair: lane x is level 0 (point q), lane y level 1 (point q + 1)
+__device__ __forceinline__ unsigned kind_bits(f2 det, float tol, int q, unsigned &degen) {
+  return kind_bits(det.v.x, tol, q, degen) | kind_bits(det.v.y, tol, q + 1, degen);
+}
+__device__ __forceinline__ double vrecip(double x) { return recip(x); }
+__device__ __forceinline__ float vrecip(float x) { return recip(x); }
+__device__ __forceinline__ f2 vrecip(f2 x) { return f2(recip(x.v.x), recip(x.v.y)); }
+}  // namespace prism_ref
+
 template <typename R, class Coef>
 __device__ __forceinline__ void integrate_prism_cd_ref(const prism_ref::Cols<R> &cols, const Coef &c, R tol,
                                                        R (&A)[36], R (&B)[6], unsigned &fail_mask,
                                                        unsigned &degen_mask) {
   using namespace prism_ref;
+  // fp64: one level per pass (scalar); fp32: both levels per pass (FFMA2 pairs)
+  using V = std::conditional_t<sizeof(R) == 8, R, f2>;
+  constexpr int NZ = Lanes<V>::NZ;
   constexpr double w = S::w(0);
   // coefficient row: c00 .. c33, d0 .. d3 (problems.py:136-140)
-  auto d = [&](int k) { return c[16 + k]; };
+  auto cv = [&](int k) { return V(c[k]); };
+  auto d = [&](int k) { return V(c[16 + k]); };
   const auto &J2 = cols.J2;
   const auto &J01 = cols.J01;
-  // per-level sums [z]; SYY / SbY carry the same weight on both levels
-  R SXX[2][3][3], SXY[2][3][3], SYX[2][3][3], SbX[2][3];
-  R SYY[6], SbY[3];
-  static_for<2>([&](auto zc) {
+  // per-pass sums [pass]; SYY / SbY carry the same weight on both levels
+  V SXX[NZ][3][3], SXY[NZ][3][3], SYX[NZ][3][3], SbX[NZ][3];
+  V SYY[6], SbY[3];
+  static_for<NZ>([&](auto zc) {
     FEK_CI(z, zc);
+    // J columns 0/1 of this pass (pairs: (level 0, level 1))
+    V Jz[3][2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if constexpr (NZ == 2) {
+          Jz[i][k] = V(J01[z][i][k]);
+        } else {
+          Jz[i][k] = V(J01[0][i][k], J01[1][i][k]);
+        }
+      }
     static_for<3>([&](auto tc) {
       FEK_CI(t, tc);
-      constexpr int Q = 2 * t + z;
-      constexpr bool F = (t == 0);           // first point of the level
+      constexpr int Q = 2 * t + z;           // pairs: lane x = q, lane y = q + 1
+      constexpr bool F = (t == 0);           // first point of the pass
       constexpr bool F2 = (t == 0 && z == 0);  // first point overall
-      R adj[3][3];
-      const R det = adjugate(J01[z], J2[t], adj);
-      const int kind = classify(det, tol);
-      fail_mask |= static_cast<unsigned>(kind != 0) << Q;
-      degen_mask |= static_cast<unsigned>(kind == KIND_DEGENERATE) << Q;
-      const R rdet = recip(det);
+      const V Jt[3] = {V(J2[t][0]), V(J2[t][1]), V(J2[t][2])};
+      V adj[3][3];
+      const V det = adjugate(Jz, Jt, adj);
+      fail_mask |= kind_bits(det, tol, Q, degen_mask);
+      const V rdet = vrecip(det);
       // K (w folded into the final weights): K00 = det c00, K0l = c0. adj_l, Kk0 = adj_k c.0,
       // Kkl = adj_k C adj_l^T / det
-      R K[4][4];
-      K[0][0] = det * c[0];
+      V K[4][4];
+      K[0][0] = det * cv(0);
 #pragma unroll
       for (int l = 0; l < 3; ++l) {
-        K[0][1 + l] = fma(c[1], adj[l][0], fma(c[2], adj[l][1], c[3] * adj[l][2]));
-        K[1 + l][0] = fma(adj[l][0], c[4], fma(adj[l][1], c[8], adj[l][2] * c[12]));
+        K[0][1 + l] = fma(cv(1), adj[l][0], fma(cv(2), adj[l][1], cv(3) * adj[l][2]));
+        K[1 + l][0] = fma(adj[l][0], cv(4), fma(adj[l][1], cv(8), adj[l][2] * cv(12)));
       }
 #pragma unroll
       for (int l = 0; l < 3; ++l) {
-        R M[3];  // M[i] = sum_j C[1+i][1+j] adj[l][j]
+        V M[3];  // M[i] = sum_j C[1+i][1+j] adj[l][j]
 #pragma unroll
         for (int i = 0; i < 3; ++i)
-          M[i] = fma(c[4 * (1 + i) + 1], adj[l][0], fma(c[4 * (1 + i) + 2], adj[l][1], c[4 * (1 + i) + 3] * adj[l][2]));
+          M[i] = fma(cv(4 * (1 + i) + 1), adj[l][0], fma(cv(4 * (1 + i) + 2), adj[l][1], cv(4 * (1 + i) + 3) * adj[l][2]));
 #pragma unroll
         for (int k = 0; k < 3; ++k) K[1 + k][1 + l] = rdet * fma(adj[k][0], M[0], fma(adj[k][1], M[1], adj[k][2] * M[2]));
       }
-      constexpr R L[3] = {R(lam(t, 0)), R(lam(t, 1)), R(lam(t, 2))};
+      const V L[3] = {V(R(lam(t, 0))), V(R(lam(t, 1))), V(R(lam(t, 2)))};
       // XX: v_a' = K[0:3][0:3] X_a', then SXX[a][a'] (+)= X_a . v_a'
       static_for<3>([&](auto apc) {
         FEK_CI(ap, apc);
-        R v[3];
+        V v[3];
 #pragma unroll
-        for (int al = 0; al < 3; ++al) v[al] = xdot<ap, true>(R(0), L[ap], K[al][0], K[al][1], K[al][2]);
+        for (int al = 0; al < 3; ++al) v[al] = xdot<ap, true>(V(R(0)), L[ap], K[al][0], K[al][1], K[al][2]);
         static_for<3>([&](auto ac) {
           FEK_CI(a, ac);
           SXX[z][a][ap] = xdot<a, F>(SXX[z][a][ap], L[a], v[0], v[1], v[2]);
@@ -694,8 +766,8 @@ __device__ __forceinline__ void integrate_prism_cd_ref(const prism_ref::Cols<R> 
       // XY / YX / YY
       static_for<3>([&](auto ac) {
         FEK_CI(a, ac);
-        const R p = xdot<a, true>(R(0), L[a], K[0][3], K[1][3], K[2][3]);  // X_a . K[:,3]
-        const R q = xdot<a, true>(R(0), L[a], K[3][0], K[3][1], K[3][2]);  // K[3,:] . X_a
+        const V p = xdot<a, true>(V(R(0)), L[a], K[0][3], K[1][3], K[2][3]);  // X_a . K[:,3]
+        const V q = xdot<a, true>(V(R(0)), L[a], K[3][0], K[3][1], K[3][2]);  // K[3,:] . X_a
         static_for<3>([&](auto bc) {
           FEK_CI(ap, bc);
           mac<F>(SXY[z][a][ap], L[ap], p);
@@ -706,12 +778,12 @@ __device__ __forceinline__ void integrate_prism_cd_ref(const prism_ref::Cols<R> 
         FEK_CI(a, ac);
         static_for<3>([&](auto bc) {
           FEK_CI(ap, bc);
-          if constexpr (ap >= a) mac<F2>(SYY[sym_index(a, ap)], R(lam(t, a) * lam(t, ap)), K[3][3]);
+          if constexpr (ap >= a) mac<F2>(SYY[sym_index(a, ap)], V(R(lam(t, a) * lam(t, ap))), K[3][3]);
         });
       });
       // load: e = vol P^T d / w = (det d0, adj d[1:4])
-      const R e0 = det * d(0);
-      R e[3];
+      const V e0 = det * d(0);
+      V e[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) e[k] = fma(adj[k][0], d(1), fma(adj[k][1], d(2), adj[k][2] * d(3)));
       static_for<3>([&](auto ac) {
@@ -721,36 +793,49 @@ __device__ __forceinline__ void integrate_prism_cd_ref(const prism_ref::Cols<R> 
       });
     });
   });
+  // per-level views of the sums (pairs: lane = level)
+  auto lv = [&](const V &x, int z) -> R { return Lanes<V>::get(x, NZ == 2 ? 0 : z); };
+  auto both = [&](const V &x) -> R {
+    if constexpr (NZ == 2) {
+      return x;
+    } else {
+      return x.v.x + x.v.y;
+    }
+  };
   // A_(a,b)(a',b') = w sum_z [l_b l_b' SXX + l_b l'_b' SXY + l'_b l_b' SYX] + w l'_b l'_b' SYY
   static_for<3>([&](auto ac) {
     FEK_CI(a, ac);
     static_for<3>([&](auto bc) {
       FEK_CI(ap, bc);
       constexpr int kyy = sym_index(a, ap);
+      const R syy = both(SYY[kyy]);
       static_for<2>([&](auto b1c) {
         FEK_CI(b, b1c);
         static_for<2>([&](auto b2c) {
           FEK_CI(bp, b2c);
           constexpr double lpb = b == 0 ? -0.5 : 0.5, lpbp = bp == 0 ? -0.5 : 0.5;
-          R acc = R(w * lpb * lpbp) * SYY[kyy];
+          R acc = R(w * lpb * lpbp) * syy;
           static_for<2>([&](auto zc) {
             FEK_CI(z, zc);
+            constexpr int zi = NZ == 2 ? z : 0;
             constexpr double lb = ell(z, b), lbp = ell(z, bp);
-            acc = fma(R(w * lb * lbp), SXX[z][a][ap], acc);
-            acc = fma(R(w * lb * lpbp), SXY[z][a][ap], acc);
-            acc = fma(R(w * lpb * lbp), SYX[z][a][ap], acc);
+            acc = fma(R(w * lb * lbp), lv(SXX[zi][a][ap], z), acc);
+            acc = fma(R(w * lb * lpbp), lv(SXY[zi][a][ap], z), acc);
+            acc = fma(R(w * lpb * lbp), lv(SYX[zi][a][ap], z), acc);
           });
           A[6 * (a + 3 * b) + (ap + 3 * bp)] = acc;
         });
       });
     });
+    const R sby = both(SbY[a]);
     static_for<2>([&](auto b1c) {
       FEK_CI(b, b1c);
       constexpr double lpb = b == 0 ? -0.5 : 0.5;
-      R acc = R(w * lpb) * SbY[a];
+      R acc = R(w * lpb) * sby;
       static_for<2>([&](auto zc) {
         FEK_CI(z, zc);
-        acc = fma(R(w * ell(z, b)), SbX[z][a], acc);
+        constexpr int zi = NZ == 2 ? z : 0;
+        acc = fma(R(w * ell(z, b)), lv(SbX[zi][a], z), acc);
       });
       B[a + 3 * b] = acc;
     });
