@@ -18,6 +18,8 @@
  *                          first-error rule (element, quadrature point, kind).
  *   fek_error_detail    <- batched.py:172-177  the |det J| / tol numbers that
  *                          go into the DegenerateElement/InvertedElement text.
+ *   fek_jacobian        <- geometry.py:94-138  jacobian_affine /
+ *                          jacobian_at_point (JacobianData) of one element.
  *   fek_checksum        <- (new) per-shard verification sums reduced with
  *                          NCCL across GPUs.
  *
@@ -144,6 +146,15 @@ int fek_decode_error(unsigned long long key, int64_t *element, int32_t *point, i
  * (device memory).  Used only to format error messages. */
 int fek_error_detail(const fek_batch_desc *d, int64_t element, int32_t point,
                      double *out_det_tol, void *cuda_stream);
+
+/* The mapping Jacobian of local element `element` of d at quadrature point
+ * `point` (-1: the affine tet Jacobian), written to out20[0..19] (device
+ * memory): [0..8] dx/dxi row-major (J[i][k] = dx_i/dxi_k), [9..17] dxi/dx
+ * (adjugate / det), [18] det J, [19] the degeneracy tolerance 1e-14 diag^3.
+ * Replaces the scalar geometry helpers jacobian_affine / jacobian_at_point
+ * (pkg/src/feklab/geometry.py:94-138) for the per-element API. */
+int fek_jacobian(const fek_batch_desc *d, int64_t element, int32_t point, double *out20,
+                 void *cuda_stream);
 
 /* Verification sums over d's outputs, written to device memory:
  * out_f64[0..3] = sum A, sum b, sum |A|, sum |b| (fixed-order, deterministic);

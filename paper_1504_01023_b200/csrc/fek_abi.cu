@@ -268,27 +268,56 @@ int fek_decode_error(unsigned long long key, int64_t *element, int32_t *point, i
   return FEK_OK;
 }
 
-int fek_error_detail(const fek_batch_desc *d, int64_t element, int32_t point, double *out_det_tol,
-                     void *cuda_stream) {
+}  // extern "C"
+
+// one-thread element queries (templates: C++ linkage)
+template <template <typename, int> class Kern>
+static int element_query(const fek_batch_desc *d, int64_t element, int32_t point, double *out, void *cuda_stream) {
   if (int rc = validate(d, false)) return rc;
-  if (!d->geometry || !out_det_tol || element < 0 || element >= d->n_elements) return FEK_ERR_ARGUMENT;
+  if (!d->geometry || !out || element < 0 || element >= d->n_elements) return FEK_ERR_ARGUMENT;
   const int w = d->layout == FEK_ELEMENT_MAJOR ? 1 : d->lane_width;
   const int nq = n_quad(d->element);
-  if (point >= nq) return FEK_ERR_ARGUMENT;
+  if (point >= nq || point < -1) return FEK_ERR_ARGUMENT;
+  if (point < 0 && d->element != FEK_TETRAHEDRON) return FEK_ERR_ARGUMENT;  // affine path: tets only
   cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
   if (d->dtype == FEK_F64) {
     if (d->element == FEK_TETRAHEDRON)
-      fek::error_detail_kernel<double, fek::TET><<<1, 1, 0, s>>>(d->geometry, element, w, point, out_det_tol);
+      Kern<double, fek::TET>::launch(d->geometry, element, w, point, out, s);
     else
-      fek::error_detail_kernel<double, fek::PRISM><<<1, 1, 0, s>>>(d->geometry, element, w, point, out_det_tol);
+      Kern<double, fek::PRISM>::launch(d->geometry, element, w, point, out, s);
   } else {
     if (d->element == FEK_TETRAHEDRON)
-      fek::error_detail_kernel<float, fek::TET><<<1, 1, 0, s>>>(d->geometry, element, w, point, out_det_tol);
+      Kern<float, fek::TET>::launch(d->geometry, element, w, point, out, s);
     else
-      fek::error_detail_kernel<float, fek::PRISM><<<1, 1, 0, s>>>(d->geometry, element, w, point, out_det_tol);
+      Kern<float, fek::PRISM>::launch(d->geometry, element, w, point, out, s);
   }
   FEK_CUDA(cudaGetLastError());
   return FEK_OK;
+}
+
+template <typename R, int ET>
+struct ErrorDetail {
+  static void launch(const void *g, int64_t e, int w, int q, double *out, cudaStream_t s) {
+    fek::error_detail_kernel<R, ET><<<1, 1, 0, s>>>(g, e, w, q, out);
+  }
+};
+
+template <typename R, int ET>
+struct Jacobian {
+  static void launch(const void *g, int64_t e, int w, int q, double *out, cudaStream_t s) {
+    fek::jacobian_kernel<R, ET><<<1, 1, 0, s>>>(g, e, w, q, out);
+  }
+};
+
+extern "C" {
+
+int fek_error_detail(const fek_batch_desc *d, int64_t element, int32_t point, double *out_det_tol,
+                     void *cuda_stream) {
+  return element_query<ErrorDetail>(d, element, point, out_det_tol, cuda_stream);
+}
+
+int fek_jacobian(const fek_batch_desc *d, int64_t element, int32_t point, double *out20, void *cuda_stream) {
+  return element_query<Jacobian>(d, element, point, out20, cuda_stream);
 }
 
 size_t fek_checksum_scratch_bytes(void) { return static_cast<size_t>(kSumBlocks) * (4 * 8 + 2 * 8); }

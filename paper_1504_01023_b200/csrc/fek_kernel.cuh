@@ -314,33 +314,55 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
 // error detail (message formatting only): det and tol of one element/point
 // ---------------------------------------------------------------------------
 
+// Jacobian of one element at one point (-1: the affine tet path), from its
+// staged layout: out[0..8] = J[i][k] = dx_i/dxi_k (geometry.py:107-138),
+// out[9..17] = dxi_dx[k][i] = adj[k][i] / det (the reference divides,
+// geometry.py:86), out[18] = det, out[19] = the degeneracy tolerance.
 template <typename R, int ET>
-__global__ void error_detail_kernel(const void *geometry, long long element, int lane_width, int point,
-                                    double *out) {
+__device__ void element_jacobian(const void *geometry, long long element, int lane_width, int point, double *out,
+                                 bool full) {
   constexpr int NV = Shape<ET>::NV, DS = 3 * NV;
   const R *g = static_cast<const R *>(geometry);
   R X[DS];
   const long long blk = element / lane_width, lane = element % lane_width;
   for (int d = 0; d < DS; ++d) X[d] = g[blk * lane_width * DS + d * lane_width + lane];
   const R tol = degeneracy_tolerance<R, NV>(X);
-  R det = R(0);
+  R J[3][3] = {};
   if (point < 0) {
-    R J[3][3];
     for (int i = 0; i < 3; ++i)
       for (int k = 0; k < 3; ++k) J[i][k] = X[3 * (k + 1) + i] - X[i];
-    det = invert3(J).det;
   } else {
     static_for<Shape<ET>::NQ>([&](auto qc) {
       constexpr int Q = decltype(qc)::value;
-      if (Q == point) {
-        R J[3][3];
-        point_jacobian<ET, Q>(X, J);
-        det = invert3(J).det;
-      }
+      if (Q == point) point_jacobian<ET, Q>(X, J);
     });
   }
-  out[0] = static_cast<double>(det);
-  out[1] = static_cast<double>(tol);
+  const Jac<R> jac = invert3(J);  // det, and adj * (1/det) (unused: the division below)
+  if (full) {
+    const R r1 = R(1);
+    const Jac<R> adj = invert3_with(J, jac.det, r1);  // adjugate
+    for (int i = 0; i < 3; ++i)
+      for (int k = 0; k < 3; ++k) {
+        out[3 * i + k] = static_cast<double>(J[i][k]);
+        out[9 + 3 * i + k] = static_cast<double>(adj.inv[i][k] / jac.det);
+      }
+    out[18] = static_cast<double>(jac.det);
+    out[19] = static_cast<double>(tol);
+  } else {
+    out[0] = static_cast<double>(jac.det);
+    out[1] = static_cast<double>(tol);
+  }
+}
+
+template <typename R, int ET>
+__global__ void error_detail_kernel(const void *geometry, long long element, int lane_width, int point,
+                                    double *out) {
+  element_jacobian<R, ET>(geometry, element, lane_width, point, out, false);
+}
+
+template <typename R, int ET>
+__global__ void jacobian_kernel(const void *geometry, long long element, int lane_width, int point, double *out) {
+  element_jacobian<R, ET>(geometry, element, lane_width, point, out, true);
 }
 
 }  // namespace fek

@@ -72,6 +72,20 @@ def test_descriptor_validation_without_gpu():
     assert lib.fek_host_workspace_bytes(ctypes.byref(d), 3, 1024) > 3 * 1024 * (18 + 6 + 36 + 6) * 8
 
 
+def test_jacobian_query_validated_without_gpu():
+    """fek_jacobian / fek_error_detail reject bad element / point arguments before any launch."""
+    lib = _native.load()
+    d = _native.BatchDesc()
+    d.element, d.problem, d.variant, d.geometry_path = 1, 0, 0, 1  # prism, generic
+    d.layout, d.lane_width, d.n_elements = 0, 1, 4
+    d.geometry = 256
+    for fn in (lib.fek_jacobian, lib.fek_error_detail):
+        assert fn(ctypes.byref(d), 0, 6, 512, None) == _native.ERR_ARGUMENT    # point out of range
+        assert fn(ctypes.byref(d), 0, -1, 512, None) == _native.ERR_ARGUMENT   # affine query on a prism
+        assert fn(ctypes.byref(d), 4, 0, 512, None) == _native.ERR_ARGUMENT    # element out of range
+        assert fn(ctypes.byref(d), 0, 0, None, None) == _native.ERR_ARGUMENT   # no output
+
+
 def test_v3_fields_validated_without_gpu():
     """ABI v3: misaligned tile-queue words and bad layout-conversion arguments are refused up front."""
     lib = _native.load()
