@@ -850,37 +850,50 @@ __device__ __forceinline__ void integrate_prism_cd_ref(const prism_ref::Cols<R> 
 //   XY[a][a'] = lam_a' (dlam_a . K[xi eta][zeta]) (YX = XY^T, K symmetric);
 //   YY[a][a'] = lam_a lam_a' K[zeta][zeta].
 // Load: b_(a,b) = w sum_z l_b(z) sum_t lam_a(t) det_q d0[q].
-// About 620 FP64 instructions per element instead of ~900.
+// 706 FP64 instructions per element instead of 1120 (fp32: both levels as FFMA2 pairs).
 template <typename R>
 __device__ __forceinline__ void integrate_prism_poisson_ref(const prism_ref::Cols<R> &cols, const R *d0, R tol,
                                                             R (&A)[36], R (&B)[6], unsigned &fail_mask,
                                                             unsigned &degen_mask) {
   using namespace prism_ref;
+  // fp64: one level per pass; fp32: both levels per pass on FFMA2 pairs (as integrate_prism_cd_ref)
+  using V = std::conditional_t<sizeof(R) == 8, R, f2>;
+  constexpr int NZ = Lanes<V>::NZ;
   constexpr double w = S::w(0);
   const auto &J2 = cols.J2;
   const auto &J01 = cols.J01;
-  R SK[2][3];      // sum_t (k00, k01, k11) of the (xi, eta) block, per level
-  R SXY[2][2][3];  // [z][a-1][a'] = sum_t lam_a'(t) p_a, p_1 = k02, p_2 = k12 (p_0 = -p_1 - p_2)
-  R SYY[6];        // sum_q lam_a lam_a' k22 (packed symmetric)
-  R SB[2][3];      // sum_t lam_a(t) det d0[q], per level
-  static_for<2>([&](auto zc) {
+  V SK[NZ][3];      // sum_t (k00, k01, k11) of the (xi, eta) block, per pass
+  V SXY[NZ][2][3];  // [z][a-1][a'] = sum_t lam_a'(t) p_a, p_1 = k02, p_2 = k12 (p_0 = -p_1 - p_2)
+  V SYY[6];         // sum_q lam_a lam_a' k22 (packed symmetric)
+  V SB[NZ][3];      // sum_t lam_a(t) det d0[q], per pass
+  static_for<NZ>([&](auto zc) {
     FEK_CI(z, zc);
+    V Jz[3][2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if constexpr (NZ == 2) {
+          Jz[i][k] = V(J01[z][i][k]);
+        } else {
+          Jz[i][k] = V(J01[0][i][k], J01[1][i][k]);
+        }
+      }
     static_for<3>([&](auto tc) {
       FEK_CI(t, tc);
-      constexpr int Q = 2 * t + z;
+      constexpr int Q = 2 * t + z;  // pairs: lane x = q, lane y = q + 1
       constexpr bool F = (t == 0);
       constexpr bool F2 = (t == 0 && z == 0);
-      R adj[3][3];
-      const R det = adjugate(J01[z], J2[t], adj);
-      const int kind = classify(det, tol);
-      fail_mask |= static_cast<unsigned>(kind != 0) << Q;
-      degen_mask |= static_cast<unsigned>(kind == KIND_DEGENERATE) << Q;
-      const R rdet = recip(det);
+      const V Jt[3] = {V(J2[t][0]), V(J2[t][1]), V(J2[t][2])};
+      V adj[3][3];
+      const V det = adjugate(Jz, Jt, adj);
+      fail_mask |= kind_bits(det, tol, Q, degen_mask);
+      const V rdet = vrecip(det);
       auto kdot = [&](int k, int l) {
         return rdet * fma(adj[k][0], adj[l][0], fma(adj[k][1], adj[l][1], adj[k][2] * adj[l][2]));
       };
-      const R k00 = kdot(0, 0), k01 = kdot(0, 1), k11 = kdot(1, 1);
-      const R k02 = kdot(0, 2), k12 = kdot(1, 2), k22 = kdot(2, 2);
+      const V k00 = kdot(0, 0), k01 = kdot(0, 1), k11 = kdot(1, 1);
+      const V k02 = kdot(0, 2), k12 = kdot(1, 2), k22 = kdot(2, 2);
       if constexpr (F) {
         SK[z][0] = k00;
         SK[z][1] = k01;
@@ -890,26 +903,33 @@ __device__ __forceinline__ void integrate_prism_poisson_ref(const prism_ref::Col
         SK[z][1] = SK[z][1] + k01;
         SK[z][2] = SK[z][2] + k11;
       }
-      const R dq = det * d0[Q];
+      V dq;
+      if constexpr (NZ == 2) {
+        dq = det * V(d0[Q]);
+      } else {
+        dq = det * V(d0[Q], d0[Q + 1]);
+      }
       static_for<3>([&](auto ac) {
         FEK_CI(a, ac);
-        constexpr R la = R(lam(t, a));
+        const V la = V(R(lam(t, a)));
         mac<F>(SXY[z][0][a], la, k02);
         mac<F>(SXY[z][1][a], la, k12);
         mac<F>(SB[z][a], la, dq);
         static_for<3>([&](auto bc) {
           FEK_CI(ap, bc);
-          if constexpr (ap >= a) mac<F2>(SYY[sym_index(a, ap)], R(lam(t, a) * lam(t, ap)), k22);
+          if constexpr (ap >= a) mac<F2>(SYY[sym_index(a, ap)], V(R(lam(t, a) * lam(t, ap))), k22);
         });
       });
     });
   });
+  auto lv = [&](const V &x, int z) -> R { return Lanes<V>::get(x, NZ == 2 ? 0 : z); };
   // XX[a][a'] per level from the K2 sums (dlam = (-1,-1), (1,0), (0,1))
   R XX[2][6];
   R XY[2][3][3];
   static_for<2>([&](auto zc) {
     FEK_CI(z, zc);
-    const R k00 = SK[z][0], k01 = SK[z][1], k11 = SK[z][2];
+    constexpr int zi = NZ == 2 ? z : 0;
+    const R k00 = lv(SK[zi][0], z), k01 = lv(SK[zi][1], z), k11 = lv(SK[zi][2], z);
     const R s0 = k00 + k01, s1 = k01 + k11;
     XX[z][sym_index(1, 1)] = k00;
     XX[z][sym_index(1, 2)] = k01;
@@ -919,11 +939,21 @@ __device__ __forceinline__ void integrate_prism_poisson_ref(const prism_ref::Col
     XX[z][sym_index(0, 0)] = s0 + s1;
 #pragma unroll
     for (int ap = 0; ap < 3; ++ap) {
-      XY[z][1][ap] = SXY[z][0][ap];
-      XY[z][2][ap] = SXY[z][1][ap];
-      XY[z][0][ap] = -(SXY[z][0][ap] + SXY[z][1][ap]);
+      const R p1 = lv(SXY[zi][0][ap], z), p2 = lv(SXY[zi][1][ap], z);
+      XY[z][1][ap] = p1;
+      XY[z][2][ap] = p2;
+      XY[z][0][ap] = -(p1 + p2);
     }
   });
+  R syy[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    if constexpr (NZ == 2) {
+      syy[k] = SYY[k];
+    } else {
+      syy[k] = SYY[k].v.x + SYY[k].v.y;
+    }
+  }
   // A_(a,b)(a',b') = w sum_z [l_b l_b' XX + l_b l'_b' XY[a][a'] + l'_b l_b' XY[a'][a]] + w l'_b l'_b' SYY
   static_for<3>([&](auto ac) {
     FEK_CI(a, ac);
@@ -936,7 +966,7 @@ __device__ __forceinline__ void integrate_prism_poisson_ref(const prism_ref::Col
           constexpr int r = a + 3 * b, s_ = ap + 3 * bp;
           if constexpr (s_ >= r) {
             constexpr double lpb = b == 0 ? -0.5 : 0.5, lpbp = bp == 0 ? -0.5 : 0.5;
-            R acc = R(w * lpb * lpbp) * SYY[sym_index(a, ap)];
+            R acc = R(w * lpb * lpbp) * syy[sym_index(a, ap)];
             static_for<2>([&](auto zc) {
               FEK_CI(z, zc);
               constexpr double lb = ell(z, b), lbp = ell(z, bp);
@@ -952,8 +982,8 @@ __device__ __forceinline__ void integrate_prism_poisson_ref(const prism_ref::Col
     });
     static_for<2>([&](auto b1c) {
       FEK_CI(b, b1c);
-      R acc = R(w * ell(0, b)) * SB[0][a];
-      B[a + 3 * b] = fma(R(w * ell(1, b)), SB[1][a], acc);
+      R acc = R(w * ell(0, b)) * lv(SB[0][a], 0);
+      B[a + 3 * b] = fma(R(w * ell(1, b)), lv(SB[NZ == 2 ? 1 : 0][a], 1), acc);
     });
   });
 }
@@ -997,7 +1027,7 @@ __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef,
 #pragma unroll
   for (int i = 0; i < NS; ++i) B[i] = R(0);
 
-  if constexpr (VAR == QSS && ET == PRISM && (!SYM || sizeof(R) == 8)) {
+  if constexpr (VAR == QSS && ET == PRISM) {
     prism_ref::Cols<R> cols;
     {
       R X[DSG];

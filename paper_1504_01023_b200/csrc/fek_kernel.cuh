@@ -62,8 +62,7 @@ struct Traits {
   static constexpr bool LAZY_X = (GEO == GEO_GENERIC) && (ET == PRISM || VAR != QSS);
   // reference-frame prism kernels (fek_element.cuh integrate_prism_qss): the
   // staged tile is only read by the prologue (C row, distinct Jacobian columns)
-  static constexpr bool PRISM_REF = (ET == PRISM && GEO == GEO_GENERIC && VAR == QSS &&
-                                     (PB == CONV_DIFF || sizeof(R) == 8));
+  static constexpr bool PRISM_REF = (ET == PRISM && GEO == GEO_GENERIC && VAR == QSS);
   // fp64: release the input stage after the prologue, so the refill's loads
   // overlap this tile's math (C4 2.175 -> 2.070 ms, C3 -1%; fp32 prism CDR,
   // with two stages, is 1% slower this way)
