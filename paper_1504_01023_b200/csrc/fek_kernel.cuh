@@ -67,6 +67,10 @@ struct Traits {
   // overlap this tile's math (C4 2.175 -> 2.070 ms, C3 -1%; fp32 prism CDR,
   // with two stages, is 1% slower this way)
   static constexpr bool EARLY_RELEASE = PRISM_REF && sizeof(R) == 8;
+  // fp32 prism Poisson (reference frame, 111 registers): 4 CTAs x 2 stages, C3 fp32 0.169 ms vs
+  // 0.191 (3 x 1), 0.175 (early release, 3 or 4 CTAs); fp64 prism Poisson at 2 CTAs x 2 stages
+  // (244 registers, no spill) is 4% slower than 3 x 1 with early release
+  static constexpr bool P32 = (sizeof(R) == 4 && ET == PRISM && PB == POISSON && PRISM_REF);
   // stages / resident CTAs: memory-bound tets keep >= 64 KB of loads in
   // flight per SM; the prism kernels spend shared memory on resident warps
   // (latency hiding for the FP64 pipe) rather than on a second stage
@@ -75,9 +79,11 @@ struct Traits {
   static constexpr bool PRISM_P = (ET == PRISM && PB == POISSON);
   // fp32 prism CDR (168 registers, half the smem) fits 3 CTAs with 2 stages
   static constexpr bool F32_PRISM_CD = (sizeof(R) == 4 && ET == PRISM && PB == CONV_DIFF);
-  static constexpr int STAGES = F32_PRISM_CD ? 2 :
+  static constexpr int STAGES_ = F32_PRISM_CD ? 2 :
       ((PRISM_P || (LAZY_X && PB == CONV_DIFF)) ? 1 : ((ET == TET && PB == POISSON) ? 3 : 2));
-  static constexpr int MIN_BLOCKS = (F32_PRISM_CD || PRISM_P || (ET == TET && PB == POISSON)) ? 3 : 2;
+  static constexpr int MIN_BLOCKS_ = (F32_PRISM_CD || PRISM_P || (ET == TET && PB == POISSON)) ? 3 : 2;
+  static constexpr int STAGES = P32 ? 2 : STAGES_;
+  static constexpr int MIN_BLOCKS = P32 ? 4 : MIN_BLOCKS_;
   static constexpr unsigned GEO_TILE_BYTES = TILE * DSG * sizeof(R);
   static constexpr unsigned COEF_TILE_BYTES = TILE * DSC * sizeof(R);
   static constexpr unsigned OUT_A_BYTES = TILE * NA * sizeof(R);
