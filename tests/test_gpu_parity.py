@@ -163,6 +163,57 @@ def test_geometry_errors_match_reference():
     assert checked >= 40
 
 
+def test_geometry_errors_fp32_locate_the_same_failure():
+    """fp32 kernels (the prism ones run the two zeta levels as one FFMA2 pair) locate the reference's
+    failure on the golden error batches: same element always; same kind and point for inverted
+    elements.  An exactly degenerate element has det J = 0 only to fp32 rounding (1e-14 diag^3 is
+    below fp32 resolution), so there fp32 may report it as inverted, or at another point."""
+    import torch
+
+    checked = 0
+    for z, name, et, pb, geo, cof in _error_cases():
+        dbatch = DeviceBatch.from_host(ElementBatch.from_arrays(et, pb, geo, cof), dtype=torch.float32)
+        for desc in case_descriptors(et, pb):
+            want = tuple(int(x) for x in z[f"{name}__{desc.short_name()}"])
+            with pytest.raises(fek.GeometryError) as err:
+                integrate_batch(desc, dbatch)
+            kind = 1 if isinstance(err.value, fek.DegenerateElement) else 2
+            point = -1 if err.value.point_index is None else err.value.point_index
+            if want[0] == 2:
+                assert (kind, err.value.element_index, point) == want, (name, desc.short_name())
+            else:
+                assert err.value.element_index == want[1], (name, desc.short_name())
+            checked += 1
+    assert checked >= 20
+
+
+def test_prism_inverted_on_the_upper_level_only():
+    """A prism whose top triangle is mirrored is inverted at the three upper-level points only
+    (q = 1, 3, 5): the reported point is 1 in fp64 and fp32 (lane y of the fp32 level pairs),
+    for every descriptor, as the oracle's first-error rule says."""
+    import torch
+
+    from oracle import numpy_oracle as O
+    from paper_1504_01023_b200.verify import random_coefficients, random_prism_geometry
+
+    rng = np.random.default_rng(77)
+    et, pb = ElementType.PRISM, ProblemClass.CONV_DIFF
+    elems = [(random_prism_geometry(rng), random_coefficients(pb, et, rng)) for _ in range(300)]
+    coords = et.reference_vertices.copy()
+    coords[[4, 5]] = coords[[5, 4]]  # mirrored top triangle: the upper points invert
+    elems[137] = (fek.ElementGeometry(et, coords), elems[137][1])
+    batch = fek.build_batch(elems)
+    for desc in case_descriptors(et, pb):
+        with pytest.raises(O.OracleGeometryError) as ref:
+            O.integrate(desc.variant.value, desc.geometry_path.value, pb.value, et.value,
+                        batch.geometry_rows(), batch.coefficient_rows())
+        assert (ref.value.kind, ref.value.element_index, ref.value.point_index) == ("inverted", 137, 1)
+        for dt in (torch.float64, torch.float32):
+            with pytest.raises(fek.InvertedElement) as err:
+                integrate_batch(desc, DeviceBatch.from_host(batch, dtype=dt))
+            assert (err.value.element_index, err.value.point_index) == (137, 1), (desc.short_name(), dt)
+
+
 def test_shape_mismatch_and_descriptor_errors():
     z, batch = corpus(TET, POISSON)
     with pytest.raises(fek.ShapeMismatch):
