@@ -2,18 +2,20 @@
 //
 // One CTA = 128 threads (4 warps) = one tile of TILE = 128 elements at a
 // time, one element per thread.  CTAs are persistent (grid = SMs x resident
-// CTAs) and walk tiles t = blockIdx.x + i*gridDim.x.  Per tile i:
+// CTAs) and take tiles from a device queue (atomicAdd; static round-robin
+// t = blockIdx.x + i*gridDim.x without one).  Per tile i:
 //
 //   1. the tile's geometry and coefficient byte ranges (contiguous in both
 //      the element-major and the lane-interleaved layout, because TILE is a
 //      multiple of every lane width) arrive by 1-D TMA bulk copies into stage
 //      i % STAGES; completion is counted on full[stage] (arrival + bytes);
 //   2. each thread pulls its element's rows into registers (conflict-free
-//      rotated 16-byte reads, fek_device.cuh) -- or, on the FP64-bound prism
-//      path, only the coefficients, re-reading the vertex coordinates from
-//      the staged tile when the Jacobian columns are formed;
+//      rotated 16-byte reads, fek_device.cuh); the QSS prism kernels read
+//      the coefficient row and form the 21 distinct Jacobian entries from
+//      the staged coordinates (their prologue);
 //   3. once every thread is done with the stage (CTA barrier), thread 0
-//      refills it with tile i + STAGES;
+//      refills it with tile i + STAGES -- for the fp64 QSS prism kernels
+//      right after the prologue, so the refill overlaps the math;
 //   4. the element math runs in registers (fek_element.cuh);
 //   5. A and b rows are written to one shared output tile (the exact global
 //      byte image) and leave the SM as two TMA bulk stores (full-line
@@ -22,9 +24,9 @@
 //
 // The barriers keep the four warps in step.  A warp-decoupled variant
 // (per-warp mbarrier release + per-warp output slices) was measured slower on
-// every case -- up to 12% on the FP64-bound prism kernel, whose ~60 KB of
-// unrolled SASS thrashes the instruction cache once warps drift apart
-// (DESIGN.md section 6).  Geometry failures become one 64-bit key per element,
+// every case -- up to 12% on the FP64-bound prism kernel, whose unrolled SASS
+// thrashes the instruction cache once warps drift apart; per-warp output
+// stores alone gained nothing.  Geometry failures become one 64-bit key per element,
 // merged with atomicMin into the caller's error word.
 #pragma once
 
