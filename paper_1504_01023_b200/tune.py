@@ -14,7 +14,8 @@ is the reference CLI's single-descriptor layout/worker sweep.
 
 Inputs are generated in HBM by the device mesh generator (``mesh.device_config``)
 and re-laid-out on the device.  Each point is the median of ``repeats``
-CUDA-event-timed launches.  The model bound is the reference's
+CUDA-event-timed launches, each queued behind an untimed one so the events
+bracket the kernel rather than the host-side call overhead.  The model bound is the reference's
 ``time_bound`` (``perfmodel.py:93-102``) with a B200 profile built from the
 MEASURED copy bandwidth and FP64 FMA peak.
 """
@@ -84,6 +85,7 @@ def sweep(case: str, n_elements: int | None = None, repeats: int = 5, widths=(1,
                 times = []
                 for _ in range(repeats):
                     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    integrate_batch(desc, batch, check=False, out=(A, b))  # keeps the stream busy
                     s.record()
                     integrate_batch(desc, batch, check=False, out=(A, b))
                     e.record()
