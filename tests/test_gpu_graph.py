@@ -48,3 +48,46 @@ def test_capture_and_replay(et, pb):
         want = integrate_batch(desc, DeviceBatch.from_host(ElementBatch.from_arrays(et, pb, g_k, c_k)))
         assert torch.equal(res.stiffness, want.stiffness) and torch.equal(res.load, want.load)
         assert int(res.error_word.item()) == -1
+
+
+def test_bench_graph_timing_does_every_step():
+    """bench.time_graph: the timed graph replays all K launches over the whole batch.
+
+    Each launcher's outputs are poisoned before the timed replay; afterwards every
+    buffer set must hold the eager result bit for bit (no launch skipped or cut
+    short), the tile queues must be back at zero, and the replay must take at
+    least K x the single-launch time floor of a real kernel.
+    """
+    import torch
+
+    import bench
+    from paper_1504_01023_b200 import KernelDescriptor, mesh, natural_path
+    from paper_1504_01023_b200.problems import Variant
+
+    cfg = mesh.bench_configs()["C1"]
+    et, pb = cfg.spec.element_type, cfg.problem
+    desc = KernelDescriptor(Variant.QSS, natural_path(et), pb, et)
+    geo, cof = mesh.device_config(cfg)
+    launchers = [bench.Launcher(desc, geo, cof), bench.Launcher(desc, geo.clone(), cof.clone())]
+    launchers[0]()
+    torch.cuda.synchronize()
+    want_A, want_b = launchers[0].A.clone(), launchers[0].b.clone()
+
+    null_ctx = bench._Null
+
+    class Poison(null_ctx):
+        def __enter__(self):  # runs right before the timed replay
+            for L in launchers:
+                L.A.fill_(float("nan"))
+                L.b.fill_(float("nan"))
+            torch.cuda.synchronize()
+            return self
+
+    steps = 6
+    ms = bench.time_graph(launchers, steps, 3, sampler=Poison())
+    for L in launchers:
+        assert torch.equal(L.A, want_A) and torch.equal(L.b, want_b)
+        assert L.error_key() == 0xFFFFFFFFFFFFFFFF
+        assert L.sched.tolist() == [0, 0]
+    # 303 MB per launch cannot move faster than ~8 TB/s
+    assert ms / steps >= 0.030, ms
