@@ -244,7 +244,7 @@ def time_launches(launchers, steps, warmup, sampler=None):
     return per, t_all[0].elapsed_time(t_all[1])
 
 
-def time_graph(launchers, steps, warmup, sampler=None):
+def time_graph(launchers, steps, warmup, sampler=None, barrier=None):
     """Device time (ms) of `steps` launches cycling through `launchers`, replayed as one CUDA graph.
 
     `warmup` eager launches, then the `steps` launches are captured on a side
@@ -254,6 +254,7 @@ def time_graph(launchers, steps, warmup, sampler=None):
     only by the GPU's own kernel-to-kernel gap (per-launch events on an eager
     stream add 3-5 us per launch: C1 53.7 vs 48.6 us).  `launchers` are
     Launcher objects or callables whose Launchers are listed in `.launchers`.
+    `barrier` (multi-rank runs) is called right before the timed replay.
     """
     import torch
 
@@ -269,13 +270,17 @@ def time_graph(launchers, steps, warmup, sampler=None):
         o.stream = st.cuda_stream
     try:
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=st):
+        # thread_local: other threads (the NCCL watchdog under torchrun) may query events meanwhile
+        with torch.cuda.graph(g, stream=st, capture_error_mode="thread_local"):
             for k in range(steps):
                 launchers[k % len(launchers)]()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(st):  # replay() launches on the current stream
             g.replay()
             st.synchronize()
+            if barrier is not None:
+                barrier()
+                torch.cuda.synchronize()
             with (sampler if sampler is not None else _Null()):
                 s.record(st)
                 g.replay()
@@ -391,7 +396,7 @@ def c5_parts(world: int, rank: int):
     return parts
 
 
-def measure_c5(steps, warmup, world=1, rank=0, sampler=None):
+def measure_c5(steps, warmup, world=1, rank=0, sampler=None, barrier=None):
     """C5: 64M-element mixed CDR mesh = one tet batch + one prism batch, range-sharded.
 
     A step integrates this rank's shard of both batches.  Inputs are generated
@@ -431,9 +436,15 @@ def measure_c5(steps, warmup, world=1, rank=0, sampler=None):
         LP()
         cur.wait_stream(side)
 
-    modes = {"serial": time_graph([serial], steps, warmup, sampler) / steps,
+    modes = {"serial": time_graph([serial], steps, warmup, sampler, barrier) / steps,
              "serial_eager": time_launches([serial], steps, warmup)[1] / steps,
              "overlap_eager": time_launches([overlap], steps, warmup)[1] / steps}
+    if barrier is not None:  # multi-rank: every rank picks the same schedule (slowest rank per schedule)
+        import torch.distributed as dist
+
+        t = torch.tensor(list(modes.values()), dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        modes = dict(zip(modes, t.tolist()))
     best = min(modes, key=modes.get)
     if best != "serial" and sampler is not None:  # re-time the winner under the clock sampler
         modes[best] = time_launches([serial if best == "serial_eager" else overlap], steps, warmup, sampler)[1] / steps
@@ -512,7 +523,7 @@ def run_ours(args) -> int:
         dist.barrier()
     torch.cuda.synchronize()
     sampler = ClockSampler(local, period=0.0005)
-    total_ms = time_graph([launcher], args.steps, args.warmup, sampler)
+    total_ms = time_graph([launcher], args.steps, args.warmup, sampler, barrier=dist.barrier if distributed else None)
     per, eager_ms = time_launches([launcher], args.steps, args.warmup)   # eager stream, for reference
     key = launcher.error_key()
     if key != 0xFFFFFFFFFFFFFFFF:
@@ -666,7 +677,7 @@ def run_c5(args) -> int:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist.barrier()
     sampler = ClockSampler(local, period=0.0005)
-    rec = measure_c5(args.steps, args.warmup, world, rank, sampler)
+    rec = measure_c5(args.steps, args.warmup, world, rank, sampler, barrier=dist.barrier if distributed else None)
     t = torch.tensor([rec["ms_per_step"]], dtype=torch.float64, device="cuda")
     if distributed:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
