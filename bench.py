@@ -354,7 +354,10 @@ def measure_case(key, steps, warmup, variant="qss"):
     launchers = [Launcher(desc, geo, cof, packed_layout=pk, dynamic=dynamic)]
     for _ in range(sets - 1):
         launchers.append(Launcher(desc, geo.clone(), cof.clone(), packed_layout=pk, dynamic=dynamic))
-    ms_graph = time_graph(launchers, steps, warmup) / steps
+    from paper_1504_01023_b200.measure import ClockSampler
+
+    sampler = ClockSampler(torch.cuda.current_device(), period=0.0005)
+    ms_graph = time_graph(launchers, steps, warmup, sampler) / steps
     per, _ = time_launches(launchers, steps, warmup)       # eager stream, events around each launch
     for L in launchers:
         if L.error_key() != 0xFFFFFFFFFFFFFFFF:
@@ -370,7 +373,7 @@ def measure_case(key, steps, warmup, variant="qss"):
         "value": n / (ms / 1e3), "unit": UNIT, "ms_per_launch": ms, "timing": "CUDA graph of the timed launches",
         "eager": {"ms_per_launch_mean": float(np.mean(per)), "ms_per_launch_min": float(np.min(per)),
                   "timing": "eager stream, CUDA events around each launch"},
-        "buffer_sets": sets,
+        "buffer_sets": sets, "clocks": sampler.summary(),
         "roofline": dict(case_roofline(et, pb, n, ms / 1e3, rb),
                          traffic=load_profile_traffic(f"{desc.short_name()}_{'f32' if fp32 else 'f64'}")),
         "parity": {"max_rel_frobenius": err, "elements_checked": cnt, "tolerance": tol, "pass": err <= tol,
@@ -414,6 +417,10 @@ def measure_c5(steps, warmup, world=1, rank=0, sampler=None, barrier=None):
     from paper_1504_01023_b200.kernels.counts import algorithmic_bytes, algorithmic_flops
     from paper_1504_01023_b200.measure import flop_peak, hbm_peak
 
+    if sampler is None:
+        from paper_1504_01023_b200.measure import ClockSampler
+
+        sampler = ClockSampler(torch.cuda.current_device(), period=0.0005)
     launchers, parts = [], c5_parts(world, rank)
     for cfg, desc, lo, n in parts:
         geo, cof = mesh.device_config(cfg, lo, n)
@@ -467,7 +474,7 @@ def measure_c5(steps, warmup, world=1, rank=0, sampler=None, barrier=None):
         parity[cfg.key] = {"max_rel_frobenius": err, "elements_checked": cnt, "pass": err <= 1e-12}
     rec = {"workload": "C5: 64,156,250-element mixed CDR mesh (175^3x6 tets + 4000^2x2 jittered prisms)",
            "elements_this_rank": n_local, "ms_per_step": ms, "value_this_rank": n_local / (ms / 1e3),
-           "schedule": best, "ms_per_step_by_schedule": modes,
+           "schedule": best, "ms_per_step_by_schedule": modes, "clocks": sampler.summary(),
            "roofline": {"bound": "concurrent max(sum bytes/HBM, sum flops/FP64)", "roof_ms": t_roof * 1e3,
                         "frac": t_roof / (ms / 1e3), "serialized_by_type_roof_ms": serial * 1e3,
                         "frac_of_serialized": serial / (ms / 1e3)},

@@ -1,0 +1,9 @@
+# round-end check, as the driver runs it: GPU tests, smoke(), both bench arms (default flags)
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+tail -2 gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
+timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; echo bench_ref=$?
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo bench=$?
+grep -h '^{' gpurun_out/bench.log > gpurun_out/bench_line.json
+grep -h '^{' gpurun_out/bench_ref.log > gpurun_out/bench_ref_line.json
