@@ -14,6 +14,9 @@
  *                          whole, on HOST arrays (ElementBatch.geometry_data /
  *                          coefficient_data in, BatchResult.stiffness / load
  *                          out): chunked H2D -> kernel -> D2H pipeline.
+ *   fek_classify        <- batched.py:136-177  _bbox_scale + _adjugate +
+ *                          _check_dets with the reference's rounding: the exact
+ *                          first-error key when fek_integrate reports NEAR.
  *   fek_decode_error    <- errors.py:8-27 + batched.py:166-177,593-599  the
  *                          first-error rule (element, quadrature point, kind).
  *   fek_error_detail    <- batched.py:172-177  the |det J| / tol numbers that
@@ -49,7 +52,7 @@
 extern "C" {
 #endif
 
-#define FEK_ABI_VERSION 3
+#define FEK_ABI_VERSION 4
 
 /* enums mirror the Python ones (refelem.py:29, problems.py:26-49) */
 enum fek_element { FEK_TETRAHEDRON = 0, FEK_PRISM = 1 };
@@ -77,7 +80,13 @@ enum fek_status {
 #define FEK_NO_ERROR 0xFFFFFFFFFFFFFFFFull
 #define FEK_KIND_DEGENERATE 1
 #define FEK_KIND_INVERTED 2
-#define FEK_KIND_PIPELINE_TIMEOUT 3
+#define FEK_KIND_PIPELINE_TIMEOUT 3 /* recorded just before the kernel traps (internal error) */
+/* The integration kernels classify on their own FMA-contracted det J against
+ * 16 x the degeneracy tolerance; the reference rounds det J differently
+ * (batched.py:151-163).  Beyond that bound both dets give the same class; within
+ * it (never on a valid mesh) the kernel records NEAR at the element's first such
+ * point and the caller re-derives the exact key with fek_classify. */
+#define FEK_KIND_NEAR 4
 
 typedef struct fek_batch_desc {
   int32_t element;        /* enum fek_element                                   */
@@ -132,11 +141,23 @@ int fek_launch_config(const fek_batch_desc *d, int *grid, int *block, int *smem_
  * from the device workspace: chunk i is copied H2D, integrated and copied D2H
  * on streams[i % n_streams], so the copy engines and the SMs overlap.
  * Blocks until done.  On a geometry failure returns FEK_ERR_GEOMETRY and
- * stores the error key in *error_key_out (FEK_NO_ERROR otherwise). */
+ * stores the error key in *error_key_out (FEK_NO_ERROR otherwise); NEAR keys
+ * are resolved internally (the geometry streams once more through the
+ * workspace into fek_classify), so the key is never FEK_KIND_NEAR. */
 size_t fek_host_workspace_bytes(const fek_batch_desc *d, int n_streams, int64_t chunk_elements);
 int fek_integrate_host(const fek_batch_desc *d, void *device_workspace, size_t workspace_bytes,
                        int n_streams, void *const *cuda_streams, int64_t chunk_elements,
                        unsigned long long *error_key_out);
+
+/* The exact first-error key of d's geometry (device pointer, d's layout and
+ * base_index; coefficients/outputs unused): every element's det J at the affine
+ * point (geo_linear) or at every quadrature point in order (geo_generic), with
+ * the reference's Jacobian, unfused adjugate det and once-rounded tolerance
+ * 1e-14 diag^3 (batched.py:136-177), merged with atomicMin into *d->error_key
+ * (caller resets it to FEK_NO_ERROR first).  Geometry-only pass, stream-ordered.
+ * Call it when fek_integrate's key decodes to FEK_KIND_NEAR; the result is then
+ * FEK_NO_ERROR (the batch is valid) or a DEGENERATE / INVERTED key. */
+int fek_classify(const fek_batch_desc *d, void *cuda_stream);
 
 /* Split an error key.  point = -1 on the element-constant (geo_linear) path. */
 int fek_decode_error(unsigned long long key, int64_t *element, int32_t *point, int32_t *kind);

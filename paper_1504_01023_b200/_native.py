@@ -19,11 +19,11 @@ if os.environ.get("FEK_LIB_OVERRIDE"):  # kernel-tuning experiments only
     LIB_PATH = os.path.abspath(os.environ["FEK_LIB_OVERRIDE"])
 HEADER_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "fek.h")
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 NO_ERROR = 0xFFFFFFFFFFFFFFFF
 
 OK, ERR_ARGUMENT, ERR_ALIGNMENT, ERR_CUDA, ERR_WORKSPACE, ERR_GEOMETRY = range(6)
-KIND_DEGENERATE, KIND_INVERTED, KIND_PIPELINE_TIMEOUT = 1, 2, 3
+KIND_DEGENERATE, KIND_INVERTED, KIND_PIPELINE_TIMEOUT, KIND_NEAR = 1, 2, 3, 4
 
 # enum codes (fek.h)
 ELEMENT = {"tet": 0, "prism": 1}
@@ -74,6 +74,7 @@ SIGNATURES = {
                                           ctypes.c_int64, ctypes.POINTER(ctypes.c_ulonglong)]),
     "fek_decode_error": (ctypes.c_int, [ctypes.c_ulonglong, ctypes.POINTER(ctypes.c_int64),
                                         ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
+    "fek_classify": (ctypes.c_int, [_DP, _P]),
     "fek_error_detail": (ctypes.c_int, [_DP, ctypes.c_int64, ctypes.c_int32, _P, _P]),
     "fek_jacobian": (ctypes.c_int, [_DP, ctypes.c_int64, ctypes.c_int32, _P, _P]),
     "fek_checksum_scratch_bytes": (ctypes.c_size_t, []),

@@ -1,4 +1,4 @@
-"""Build libfek.so (sm_100a) in-tree, and the C oracle used by the tests.
+"""Build libfek.so (sm_100a) in-tree.
 
     python -m paper_1504_01023_b200.build_native [--force] [-j N]
 
@@ -104,23 +104,6 @@ def build_library(force: bool = False, jobs: int | None = None, verbose: bool = 
     return LIB
 
 
-def build_oracle(force: bool = False) -> str | None:
-    """Compile oracle/fek_oracle.c (test infrastructure) if present."""
-    src = os.path.join(ROOT, "oracle", "fek_oracle.c")
-    if not os.path.exists(src):
-        return None
-    out_dir = os.path.join(ROOT, "oracle", "_build")
-    os.makedirs(out_dir, exist_ok=True)
-    lib = os.path.join(out_dir, "libfekoracle.so")
-    if force or _stale(lib, [src]):
-        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
-               src, "-o", lib, "-lm"]
-        res = subprocess.run(cmd, capture_output=True, text=True)
-        if res.returncode != 0:
-            raise RuntimeError(f"oracle build failed:\n{res.stdout}{res.stderr}")
-    return lib
-
-
 def register_report() -> list[tuple[str, int, int, int]]:
     """(kernel, registers, spill-store bytes, spill-load bytes) from the ptxas logs."""
     import re
@@ -144,9 +127,6 @@ def main(argv=None) -> int:
     args = ap.parse_args(argv)
     lib = build_library(force=args.force, jobs=args.jobs, verbose=True)
     print(lib)
-    orc = build_oracle(force=args.force)
-    if orc:
-        print(orc)
     if args.registers:
         for name, regs, ss, sl in sorted(register_report()):
             print(f"{regs:4d} regs  spill {ss:4d}/{sl:4d}  {name}")

@@ -264,7 +264,7 @@ int fek_decode_error(unsigned long long key, int64_t *element, int32_t *point, i
   const unsigned long long within = (key >> 7) & 8191ull;
   if (element) *element = static_cast<int64_t>((blk << fek::ERROR_BLOCK_SHIFT) | within);
   if (point) *point = q == 15 ? -1 : q;
-  if (kind) *kind = static_cast<int32_t>(key & 3ull);
+  if (kind) *kind = static_cast<int32_t>(key & 127ull);
   return FEK_OK;
 }
 
@@ -295,6 +295,37 @@ static int element_query(const fek_batch_desc *d, int64_t element, int32_t point
   return FEK_OK;
 }
 
+// exact classification pass (fek_classify)
+template <typename R, int ET, int GEO>
+static void launch_classify(const fek_batch_desc *d, int lane_width, int grid, cudaStream_t s) {
+  fek::classify_kernel<R, ET, GEO><<<grid, 256, 0, s>>>(d->geometry, d->n_elements, d->base_index, lane_width,
+                                                        d->error_key);
+}
+
+static int classify_batch(const fek_batch_desc *d, cudaStream_t s) {
+  if (int rc = validate(d, false)) return rc;
+  if (d->n_elements == 0) return FEK_OK;
+  if (!d->geometry || !d->error_key) return FEK_ERR_ARGUMENT;
+  int dev = 0, sms = 148;
+  FEK_CUDA(cudaGetDevice(&dev));
+  FEK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const long long blocks = (d->n_elements + 255) / 256, cap = 8ll * sms;
+  const int grid = static_cast<int>(blocks < cap ? blocks : cap);
+  const int w = d->layout == FEK_ELEMENT_MAJOR ? 1 : d->lane_width;
+  const bool lin = d->geometry_path == FEK_GEO_LINEAR;
+  if (d->dtype == FEK_F64) {
+    if (d->element == FEK_PRISM) launch_classify<double, fek::PRISM, fek::GEO_GENERIC>(d, w, grid, s);
+    else if (lin) launch_classify<double, fek::TET, fek::GEO_LINEAR>(d, w, grid, s);
+    else launch_classify<double, fek::TET, fek::GEO_GENERIC>(d, w, grid, s);
+  } else {
+    if (d->element == FEK_PRISM) launch_classify<float, fek::PRISM, fek::GEO_GENERIC>(d, w, grid, s);
+    else if (lin) launch_classify<float, fek::TET, fek::GEO_LINEAR>(d, w, grid, s);
+    else launch_classify<float, fek::TET, fek::GEO_GENERIC>(d, w, grid, s);
+  }
+  FEK_CUDA(cudaGetLastError());
+  return FEK_OK;
+}
+
 template <typename R, int ET>
 struct ErrorDetail {
   static void launch(const void *g, int64_t e, int w, int q, double *out, cudaStream_t s) {
@@ -310,6 +341,10 @@ struct Jacobian {
 };
 
 extern "C" {
+
+int fek_classify(const fek_batch_desc *d, void *cuda_stream) {
+  return classify_batch(d, static_cast<cudaStream_t>(cuda_stream));
+}
 
 int fek_error_detail(const fek_batch_desc *d, int64_t element, int32_t point, double *out_det_tol,
                      void *cuda_stream) {
@@ -479,6 +514,24 @@ int fek_integrate_host(const fek_batch_desc *d, void *device_workspace, size_t w
   cudaEventDestroy(ready);
   if (rc) return rc;
   FEK_CUDA(cudaMemcpy(error_key_out, dkey, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  if (*error_key_out != FEK_NO_ERROR && (*error_key_out & 127ull) == FEK_KIND_NEAR) {
+    // an element within 16 tol of the degeneracy bound: re-classify the whole batch with
+    // the reference's rounding, its geometry streamed once more through slot 0 (rare path)
+    FEK_CUDA(cudaMemsetAsync(dkey, 0xFF, sizeof(unsigned long long), s0));
+    char *dg = ws + header;
+    for (long long lo = 0; lo < n; lo += chunk) {
+      const long long cnt = n - lo < chunk ? n - lo : chunk;
+      FEK_CUDA(cudaMemcpyAsync(dg, hg + lo * dsg * rb, flat_len(cnt, dsg, w) * rb, cudaMemcpyHostToDevice, s0));
+      fek_batch_desc cd = *d;
+      cd.n_elements = cnt;
+      cd.base_index = d->base_index + lo;
+      cd.geometry = dg;
+      cd.error_key = dkey;
+      if (int crc = classify_batch(&cd, s0)) return crc;
+    }
+    FEK_CUDA(cudaMemcpyAsync(error_key_out, dkey, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s0));
+    FEK_CUDA(cudaStreamSynchronize(s0));
+  }
   return *error_key_out == FEK_NO_ERROR ? FEK_OK : FEK_ERR_GEOMETRY;
 }
 

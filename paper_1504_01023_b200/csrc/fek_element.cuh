@@ -42,6 +42,9 @@ constexpr unsigned long long NO_ERROR = 0xFFFFFFFFFFFFFFFFull;
 constexpr int KIND_DEGENERATE = 1;
 constexpr int KIND_INVERTED = 2;
 constexpr int KIND_PIPELINE_TIMEOUT = 3;
+// |det J| within NEAR_TOL_FACTOR * tol at the element's first flagged point: the kernels' FMA det
+// cannot decide the class the reference's way there; fek_classify re-derives the key exactly
+constexpr int KIND_NEAR = 4;
 constexpr int ERROR_BLOCK_SHIFT = 13;  // batched.py:50 BLOCK_ELEMENTS = 8192
 
 // Error key ordering = the reference's first-error rule (batched.py:528-533,
@@ -85,6 +88,19 @@ __device__ __forceinline__ R rmin(R a, R b) {
   return a < b ? a : b;
 }
 
+// s**3 rounded ONCE, as the reference's `scale**3` is a single pow() (batched.py:167,
+// geometry.py:89): s^2 = p + pe and p s = h + he exactly, so s^3 = h + (he + pe s) with only
+// the final sum rounding (a double rounding needs the tail within ~2^-100 of a tie).  The
+// naive (s*s)*s differs from the correctly rounded cube on ~26% of scales.  numpy's own
+// scale**3 is host-ISA dependent: glibc pow is correctly rounded on all but
+// ~0.1% of scales, the AVX-512 SVML pow numpy dispatches to is not on ~5%.
+template <typename R>
+__device__ __forceinline__ R cube_rn(R s) {
+  const R p = s * s, pe = fma(s, s, -p);
+  const R h = p * s, he = fma(p, s, -h);
+  return h + fma(pe, s, he);
+}
+
 // 1e-14 * (bounding-box diagonal)^3   (geometry.py:22-24, batched.py:136-148)
 template <typename R, int NV>
 __device__ __forceinline__ R degeneracy_tolerance(const R *X) {
@@ -101,7 +117,20 @@ __device__ __forceinline__ R degeneracy_tolerance(const R *X) {
     acc = (i == 0) ? span * span : acc + span * span;  // batched.py:145-147 rounding
   }
   const R scale = sqrt(acc);
-  return R(1e-14) * (scale * scale * scale);
+  return R(1e-14) * cube_rn(scale);
+}
+
+// The kernels classify on their own (FMA-contracted) det against this widened bound and leave
+// the near elements to the exact classification (classify_exact / fek_classify).
+// Both dets approximate the exact determinant within ~3 * 2^-53 * 6 M^3, M = max |J entry| <=
+// the bounding-box diagonal (tet J columns are vertex differences; prism J entries are convex
+// combinations of them, the zeta column half of one), i.e. within 0.2 tol each: beyond 16 tol
+// the fast det's class (valid / inverted) is the reference's.  Valid meshes have det ~ diag^3,
+// 1e13 tol, so the exact pass never runs on them.
+constexpr int NEAR_TOL_FACTOR = 16;
+template <typename R, int NV>
+__device__ __forceinline__ R near_bound(const R *X) {
+  return R(NEAR_TOL_FACTOR) * degeneracy_tolerance<R, NV>(X);  // exact: a power of two
 }
 
 // cofactor adjugate + determinant of J[i][k] (row i = physical x_i,
@@ -182,6 +211,59 @@ __device__ __forceinline__ int classify(R det, R tol) {
   if (fabs(det) <= tol) return KIND_DEGENERATE;
   if (det < R(0)) return KIND_INVERTED;
   return 0;
+}
+
+// the kernels' classification: near (|det| <= near_bound) first, then inverted
+template <typename R>
+__device__ __forceinline__ int classify_fast(R det, R bound) {
+  if (fabs(det) <= bound) return KIND_NEAR;
+  if (det < R(0)) return KIND_INVERTED;
+  return 0;
+}
+
+__device__ __forceinline__ double mul_rn(double x, double y) { return __dmul_rn(x, y); }
+__device__ __forceinline__ double add_rn(double x, double y) { return __dadd_rn(x, y); }
+__device__ __forceinline__ double sub_rn(double x, double y) { return __dsub_rn(x, y); }
+__device__ __forceinline__ float mul_rn(float x, float y) { return __fmul_rn(x, y); }
+__device__ __forceinline__ float add_rn(float x, float y) { return __fadd_rn(x, y); }
+__device__ __forceinline__ float sub_rn(float x, float y) { return __fsub_rn(x, y); }
+
+// The reference's adjugate and determinant rounding (batched.py:151-163 = geometry.py:62-72):
+// every product rounded, cofactors e*i - f*h, det = (a c00 + b c01) + c c02.  Never contracted.
+template <typename R>
+__device__ __forceinline__ R det_ref(const R (&J)[3][3]) {
+  const R c00 = sub_rn(mul_rn(J[1][1], J[2][2]), mul_rn(J[1][2], J[2][1]));
+  const R c01 = sub_rn(mul_rn(J[1][2], J[2][0]), mul_rn(J[1][0], J[2][2]));
+  const R c02 = sub_rn(mul_rn(J[1][0], J[2][1]), mul_rn(J[1][1], J[2][0]));
+  return add_rn(add_rn(mul_rn(J[0][0], c00), mul_rn(J[0][1], c01)), mul_rn(J[0][2], c02));
+}
+template <typename R>
+__device__ __forceinline__ void adjugate_ref(const R (&J)[3][3], R (&adj)[3][3]) {
+  auto cof = [](R x, R y, R u, R v) { return sub_rn(mul_rn(x, y), mul_rn(u, v)); };
+  const R a = J[0][0], b = J[0][1], c = J[0][2];
+  const R d = J[1][0], e = J[1][1], f = J[1][2];
+  const R g = J[2][0], h = J[2][1], i = J[2][2];
+  adj[0][0] = cof(e, i, f, h);
+  adj[0][1] = cof(c, h, b, i);
+  adj[0][2] = cof(b, f, c, e);
+  adj[1][0] = cof(f, g, d, i);
+  adj[1][1] = cof(a, i, c, g);
+  adj[1][2] = cof(c, d, a, f);
+  adj[2][0] = cof(d, h, e, g);
+  adj[2][1] = cof(b, g, a, h);
+  adj[2][2] = cof(a, e, b, d);
+}
+
+// (kind, point) of an element from per-point bitmasks: the SMALLEST flagged point, as the
+// reference checks q = 0, 1, ... in order; a near point there leaves the verdict to fek_classify
+__device__ __forceinline__ void first_failure(unsigned inverted, unsigned near, int &kind, int &point) {
+  const unsigned m = inverted | near;
+  kind = 0;
+  point = -1;
+  if (m) {
+    point = __ffs(m) - 1;
+    kind = ((near >> point) & 1u) ? KIND_NEAR : KIND_INVERTED;
+  }
 }
 
 // sum_k c_k * x_k over compile-time coefficients, skipping zeros and using
@@ -306,7 +388,7 @@ __device__ __forceinline__ void integrate_tet_linear(const R (&X)[12], const R *
 #pragma unroll
     for (int k = 0; k < 3; ++k) J[i][k] = X[3 * (k + 1) + i] - X[i];
   const Jac<R> jac = invert3(J);
-  kind = classify(jac.det, degeneracy_tolerance<R, 4>(X));
+  kind = classify_fast(jac.det, near_bound<R, 4>(X));
   const R det = jac.det;
   // g[s][i]: shape 0 has local gradient (-1,-1,-1), shape k+1 the unit e_k
   R g[4][3];
@@ -380,21 +462,21 @@ struct PointData {
   Jac<R> jac;
   R vol;
   int kind;
-  __device__ __forceinline__ PointData(const R *X, R tol) {
+  __device__ __forceinline__ PointData(const R *X, R bound) {
     R J[3][3];
     point_jacobian<ET, Q>(X, J);
-    init(J, tol);
+    init(J, bound);
   }
-  __device__ __forceinline__ PointData(const R (&J)[3][3], R tol) { init(J, tol); }
-  __device__ __forceinline__ PointData(const R (&J)[3][3], R det, R r, R tol) {
+  __device__ __forceinline__ PointData(const R (&J)[3][3], R bound) { init(J, bound); }
+  __device__ __forceinline__ PointData(const R (&J)[3][3], R det, R r, R bound) {
     jac = invert3_with(J, det, r);
-    kind = classify(det, tol);
+    kind = classify_fast(det, bound);
     constexpr R w = R(Shape<ET>::w(Q));
     vol = det * w;
   }
-  __device__ __forceinline__ void init(const R (&J)[3][3], R tol) {
+  __device__ __forceinline__ void init(const R (&J)[3][3], R bound) {
     jac = invert3(J);
-    kind = classify(jac.det, tol);
+    kind = classify_fast(jac.det, bound);
     constexpr R w = R(Shape<ET>::w(Q));
     vol = jac.det * w;
   }
@@ -430,14 +512,14 @@ struct SmemGeometry {
 // Points are visited z-major for prisms (accumulation order is free: A is
 // not bitwise-matched, only J is).
 template <typename R, int ET, class Geo, class F>
-__device__ __forceinline__ void for_each_point(const Geo &geo, R tol, F &&f) {
+__device__ __forceinline__ void for_each_point(const Geo &geo, R bound, F &&f) {
   constexpr int DSG = 3 * Shape<ET>::NV;
   if constexpr (ET == TET) {
     R X[DSG];
     geo.fetch(X);
     R J[3][3];
     point_jacobian<TET, 0>(X, J);
-    const PointData<TET, 0, R> pd(J, tol);  // w_q and J are the same at all 4 points
+    const PointData<TET, 0, R> pd(J, bound);  // w_q and J are the same at all 4 points
     static_for<4>([&](auto qc) {
       FEK_CI(Q, qc);
       f(std::integral_constant<int, Q>{}, pd);
@@ -469,7 +551,7 @@ __device__ __forceinline__ void for_each_point(const Geo &geo, R tol, F &&f) {
         const R J[3][3] = {{J01[z][0][0], J01[z][0][1], J2[t][0]},
                            {J01[z][1][0], J01[z][1][1], J2[t][1]},
                            {J01[z][2][0], J01[z][2][1], J2[t][2]}};
-        const PointData<PRISM, Q, R> pd(J, tol);
+        const PointData<PRISM, Q, R> pd(J, bound);
         f(std::integral_constant<int, Q>{}, pd);
       });
     });
@@ -673,19 +755,18 @@ struct Lanes<f2> {
   __device__ static float get(f2 x, int lane) { return lane ? x.v.y : x.v.x; }
 };
 
-__device__ __forceinline__ unsigned kind_bits(double det, double tol, int q, unsigned &degen) {
-  const int k = classify(det, tol);
-  degen |= static_cast<unsigned>(k == KIND_DEGENERATE) << q;
-  return static_cast<unsigned>(k != 0) << q;
+// classify_fast as bitmasks: returns the det < 0 bit, marks |det| <= bound as near
+__device__ __forceinline__ unsigned kind_bits(double det, double bound, int q, unsigned &near) {
+  near |= static_cast<unsigned>(fabs(det) <= bound) << q;
+  return static_cast<unsigned>(det < 0.0) << q;
 }
-__device__ __forceinline__ unsigned kind_bits(float det, float tol, int q, unsigned &degen) {
-  const int k = classify(det, tol);
-  degen |= static_cast<unsigned>(k == KIND_DEGENERATE) << q;
-  return static_cast<unsigned>(k != 0) << q;
+__device__ __forceinline__ unsigned kind_bits(float det, float bound, int q, unsigned &near) {
+  near |= static_cast<unsigned>(fabsf(det) <= bound) << q;
+  return static_cast<unsigned>(det < 0.0f) << q;
 }
 // pair: lane x is level 0 (point q), lane y level 1 (point q + 1)
-__device__ __forceinline__ unsigned kind_bits(f2 det, float tol, int q, unsigned &degen) {
-  return kind_bits(det.v.x, tol, q, degen) | kind_bits(det.v.y, tol, q + 1, degen);
+__device__ __forceinline__ unsigned kind_bits(f2 det, float bound, int q, unsigned &near) {
+  return kind_bits(det.v.x, bound, q, near) | kind_bits(det.v.y, bound, q + 1, near);
 }
 __device__ __forceinline__ double vrecip(double x) { return recip(x); }
 __device__ __forceinline__ float vrecip(float x) { return recip(x); }
@@ -693,9 +774,9 @@ __device__ __forceinline__ f2 vrecip(f2 x) { return f2(recip(x.v.x), recip(x.v.y
 }  // namespace prism_ref
 
 template <typename R, class Coef>
-__device__ __forceinline__ void integrate_prism_cd_ref(const prism_ref::Cols<R> &cols, const Coef &c, R tol,
+__device__ __forceinline__ void integrate_prism_cd_ref(const prism_ref::Cols<R> &cols, const Coef &c, R bound,
                                                        R (&A)[36], R (&B)[6], unsigned &fail_mask,
-                                                       unsigned &degen_mask) {
+                                                       unsigned &near_mask) {
   using namespace prism_ref;
   // fp64: one level per pass (scalar); fp32: both levels per pass (FFMA2 pairs)
   using V = std::conditional_t<sizeof(R) == 8, R, f2>;
@@ -731,7 +812,7 @@ __device__ __forceinline__ void integrate_prism_cd_ref(const prism_ref::Cols<R> 
       const V Jt[3] = {V(J2[t][0]), V(J2[t][1]), V(J2[t][2])};
       V adj[3][3];
       const V det = adjugate(Jz, Jt, adj);
-      fail_mask |= kind_bits(det, tol, Q, degen_mask);
+      fail_mask |= kind_bits(det, bound, Q, near_mask);
       const V rdet = vrecip(det);
       // K (w folded into the final weights): K00 = det c00, K0l = c0. adj_l, Kk0 = adj_k c.0,
       // Kkl = adj_k C adj_l^T / det
@@ -852,9 +933,9 @@ __device__ __forceinline__ void integrate_prism_cd_ref(const prism_ref::Cols<R> 
 // Load: b_(a,b) = w sum_z l_b(z) sum_t lam_a(t) det_q d0[q].
 // 706 FP64 instructions per element instead of 1120 (fp32: both levels as FFMA2 pairs).
 template <typename R>
-__device__ __forceinline__ void integrate_prism_poisson_ref(const prism_ref::Cols<R> &cols, const R *d0, R tol,
+__device__ __forceinline__ void integrate_prism_poisson_ref(const prism_ref::Cols<R> &cols, const R *d0, R bound,
                                                             R (&A)[36], R (&B)[6], unsigned &fail_mask,
-                                                            unsigned &degen_mask) {
+                                                            unsigned &near_mask) {
   using namespace prism_ref;
   // fp64: one level per pass; fp32: both levels per pass on FFMA2 pairs (as integrate_prism_cd_ref)
   using V = std::conditional_t<sizeof(R) == 8, R, f2>;
@@ -887,7 +968,7 @@ __device__ __forceinline__ void integrate_prism_poisson_ref(const prism_ref::Col
       const V Jt[3] = {V(J2[t][0]), V(J2[t][1]), V(J2[t][2])};
       V adj[3][3];
       const V det = adjugate(Jz, Jt, adj);
-      fail_mask |= kind_bits(det, tol, Q, degen_mask);
+      fail_mask |= kind_bits(det, bound, Q, near_mask);
       const V rdet = vrecip(det);
       auto kdot = [&](int k, int l) {
         return rdet * fma(adj[k][0], adj[l][0], fma(adj[k][1], adj[l][1], adj[k][2] * adj[l][2]));
@@ -991,24 +1072,19 @@ __device__ __forceinline__ void integrate_prism_poisson_ref(const prism_ref::Col
 // QSS prism kernels from the element's distinct Jacobian columns (computed by
 // the caller, so the input stage can be released before the math starts)
 template <typename R, int PB, class Coef>
-__device__ __forceinline__ void integrate_prism_qss(const prism_ref::Cols<R> &cols, const Coef &coef, R tol,
+__device__ __forceinline__ void integrate_prism_qss(const prism_ref::Cols<R> &cols, const Coef &coef, R bound,
                                                     R (&A)[36], R (&B)[6], int &kind, int &kind_point) {
-  unsigned fail_mask = 0, degen_mask = 0;
+  unsigned fail_mask = 0, near_mask = 0;
   if constexpr (PB == POISSON) {
-    integrate_prism_poisson_ref<R>(cols, coef, tol, A, B, fail_mask, degen_mask);
+    integrate_prism_poisson_ref<R>(cols, coef, bound, A, B, fail_mask, near_mask);
   } else {
-    integrate_prism_cd_ref<R>(cols, coef, tol, A, B, fail_mask, degen_mask);
+    integrate_prism_cd_ref<R>(cols, coef, bound, A, B, fail_mask, near_mask);
   }
-  kind = 0;
-  kind_point = -1;
-  if (fail_mask) {  // the SMALLEST failing point, as in the reference
-    kind_point = __ffs(fail_mask) - 1;
-    kind = ((degen_mask >> kind_point) & 1u) ? KIND_DEGENERATE : KIND_INVERTED;
-  }
+  first_failure(fail_mask, near_mask, kind, kind_point);
 }
 
 template <typename R, int ET, int PB, int VAR, class Geo, class Load>
-__device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef, const Load &load, R tol,
+__device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef, const Load &load, R bound,
                                                   R (&A)[Shape<ET>::NS * Shape<ET>::NS],
                                                   R (&B)[Shape<ET>::NS], int &kind, int &kind_point) {
   using S = Shape<ET>;
@@ -1017,10 +1093,10 @@ __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef,
   // failing points as bitmasks (branch-free); the reported point is the
   // SMALLEST failing q, as in the reference (q = 0, 1, ... checked in order;
   // prism points are visited zeta-major here)
-  unsigned fail_mask = 0, degen_mask = 0;
+  unsigned fail_mask = 0, near_mask = 0;
   auto note = [&](int k, int q) {
-    fail_mask |= static_cast<unsigned>(k != 0) << q;
-    degen_mask |= static_cast<unsigned>(k == KIND_DEGENERATE) << q;
+    fail_mask |= static_cast<unsigned>(k == KIND_INVERTED) << q;
+    near_mask |= static_cast<unsigned>(k == KIND_NEAR) << q;
   };
 #pragma unroll
   for (int i = 0; i < NS * NS; ++i) A[i] = R(0);
@@ -1035,12 +1111,12 @@ __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef,
       prism_ref::jacobian_columns(X, cols.J2, cols.J01);
     }
     if constexpr (SYM) {
-      integrate_prism_poisson_ref<R>(cols, coef, tol, A, B, fail_mask, degen_mask);
+      integrate_prism_poisson_ref<R>(cols, coef, bound, A, B, fail_mask, near_mask);
     } else {
-      integrate_prism_cd_ref<R>(cols, coef, tol, A, B, fail_mask, degen_mask);
+      integrate_prism_cd_ref<R>(cols, coef, bound, A, B, fail_mask, near_mask);
     }
   } else if constexpr (VAR == QSS) {
-    for_each_point<R, ET>(geo, tol, [&](auto qc, const auto &pd) {
+    for_each_point<R, ET>(geo, bound, [&](auto qc, const auto &pd) {
       FEK_CI(Q, qc);
       note(pd.kind, Q);
       R g[NS][3];
@@ -1085,7 +1161,7 @@ __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef,
         FEK_CI(Q, qc);
         R X[DSG];
         geo.fetch(X);
-        const PointData<ET, Q, R> pd(X, tol);
+        const PointData<ET, Q, R> pd(X, bound);
         note(pd.kind, Q);
         R g[NS][3];
         all_grads<ET, Q>(pd.jac, g);
@@ -1124,7 +1200,7 @@ __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef,
             FEK_CI(Q, qc);
             R X[DSG];
             geo.fetch(X);
-            const PointData<ET, Q, R> pd(X, tol);
+            const PointData<ET, Q, R> pd(X, bound);
             note(pd.kind, Q);
             R gr[3], gs[3];
             global_grad<ET, Q, r>(pd.jac, gr);
@@ -1152,12 +1228,7 @@ __device__ __forceinline__ void integrate_generic(const Geo &geo, const R *coef,
 #pragma unroll
       for (int s = 0; s < r; ++s) A[NS * r + s] = A[NS * s + r];
   }
-  kind = 0;
-  kind_point = -1;
-  if (fail_mask) {
-    kind_point = __ffs(fail_mask) - 1;
-    kind = ((degen_mask >> kind_point) & 1u) ? KIND_DEGENERATE : KIND_INVERTED;
-  }
+  first_failure(fail_mask, near_mask, kind, kind_point);
 }
 
 }  // namespace fek

@@ -196,12 +196,17 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
     // the end-of-work / timeout test rides on the stage-release barrier below
     // (one CTA barrier fewer per tile: C4 -1.3%, C4 fp32 -0.8%); a thread that
     // timed out may see a stale tile here, which only feeds discarded work
-    // before that barrier.  On a timeout the CTA reports and leaves through the
-    // common exit (drains bulk stores, retires the queue).
+    // before that barrier.  A timeout is fatal: bulk loads of the other stages
+    // may still be in flight into this CTA's shared memory, so leaving would let
+    // them land in a co-resident CTA's; the key is recorded, then the kernel traps.
     const bool stop = !landed || t >= pipe.tiles;
     auto release = [&]() -> bool {
       if (__syncthreads_or(stop)) {
-        if (!landed) atomicMin(p.error_key, static_cast<unsigned long long>(KIND_PIPELINE_TIMEOUT));
+        if (!landed) {
+          atomicMin(p.error_key, static_cast<unsigned long long>(KIND_PIPELINE_TIMEOUT));
+          __threadfence_system();
+          __trap();
+        }
         return false;
       }
       if (tid == 0) issue_stage(s);
@@ -219,16 +224,16 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
       // prologue from the staged tile, release the stage, then the math
       // overlaps the refill's loads
       prism_ref::Cols<R> cols;
-      R tol;
+      R bound;
       if (active) {
         RowIO<R, K::DSC>::load(pipe.coef(s), tid, p.lane_width, C);
         R X[K::DSG];
         RowIO<R, K::DSG>::load(pipe.geo(s), tid, p.lane_width, X);
-        tol = degeneracy_tolerance<R, K::NV>(X);
+        bound = near_bound<R, K::NV>(X);
         prism_ref::jacobian_columns(X, cols.J2, cols.J01);
       }
       if (!release()) break;
-      if (active) integrate_prism_qss<R, K::PB>(cols, C, tol, A, B, kind, kind_point);
+      if (active) integrate_prism_qss<R, K::PB>(cols, C, bound, A, B, kind, kind_point);
     } else if constexpr (!K::LAZY_X) {
       R X[K::DSG];
       if (active) {
@@ -240,9 +245,9 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
         if constexpr (K::GEO == GEO_LINEAR) {
           integrate_tet_linear<R, K::PB>(X, C, A, B, kind);
         } else {
-          const R tol = degeneracy_tolerance<R, K::NV>(X);
+          const R bound = near_bound<R, K::NV>(X);
           integrate_generic<R, K::ET, K::PB, K::VAR>(RegGeometry<R, K::DSG>{X}, C, RegLoad<R>{C + (K::DSC >= 20 ? 16 : 0)},
-                                                     tol, A, B, kind, kind_point);
+                                                     bound, A, B, kind, kind_point);
         }
       }
     } else {
@@ -251,8 +256,8 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
         const SmemGeometry<R, K::DSG> geo{pipe.geo(s), tid, p.lane_width};
         R X[K::DSG];
         geo.fetch(X);
-        const R tol = degeneracy_tolerance<R, K::NV>(X);
-        integrate_generic<R, K::ET, K::PB, K::VAR>(geo, C, RegLoad<R>{C + (K::DSC >= 20 ? 16 : 0)}, tol, A, B, kind,
+        const R bound = near_bound<R, K::NV>(X);
+        integrate_generic<R, K::ET, K::PB, K::VAR>(geo, C, RegLoad<R>{C + (K::DSC >= 20 ? 16 : 0)}, bound, A, B, kind,
                                                    kind_point);
       }
       if (!release()) break;
@@ -349,21 +354,72 @@ __device__ void element_jacobian(const void *geometry, long long element, int la
       if (Q == point) point_jacobian<ET, Q>(X, J);
     });
   }
-  const Jac<R> jac = invert3(J);  // det, and adj * (1/det) (unused: the division below)
+  // the reference's det and adjugate rounding (geometry.py:62-89; the classification of
+  // classify_exact), not the kernels' FMA det
+  const R det = det_ref(J);
   if (full) {
-    const R r1 = R(1);
-    const Jac<R> adj = invert3_with(J, jac.det, r1);  // adjugate
+    R adj[3][3];
+    adjugate_ref(J, adj);
     for (int i = 0; i < 3; ++i)
       for (int k = 0; k < 3; ++k) {
         out[3 * i + k] = static_cast<double>(J[i][k]);
-        out[9 + 3 * i + k] = static_cast<double>(adj.inv[i][k] / jac.det);
+        out[9 + 3 * i + k] = static_cast<double>(adj[i][k] / det);
       }
-    out[18] = static_cast<double>(jac.det);
+    out[18] = static_cast<double>(det);
     out[19] = static_cast<double>(tol);
   } else {
-    out[0] = static_cast<double>(jac.det);
+    out[0] = static_cast<double>(det);
     out[1] = static_cast<double>(tol);
   }
+}
+
+// ---------------------------------------------------------------------------
+// exact classification (fek_classify): the reference's geometry check alone
+// ---------------------------------------------------------------------------
+
+// First-error key of one element with the reference's rounding throughout: the
+// reference-exact Jacobian (jac_entry), the unfused adjugate det (det_ref) and the
+// correctly rounded tol, checked at the affine point (GEO_LINEAR, batched.py:343-349)
+// or at q = 0, 1, ... (generic paths, batched.py:193-207) -- _check_dets, :166-177.
+template <typename R, int ET, int GEO>
+__device__ __forceinline__ unsigned long long classify_exact(const R *X, long long e_abs) {
+  const R tol = degeneracy_tolerance<R, Shape<ET>::NV>(X);
+  if constexpr (GEO == GEO_LINEAR) {
+    R J[3][3];
+    point_jacobian<ET, 0>(X, J);
+    const int k = classify(det_ref(J), tol);
+    return k ? make_error_key(e_abs, -1, k) : NO_ERROR;
+  } else {
+    unsigned long long key = NO_ERROR;
+    static_for<Shape<ET>::NQ>([&](auto qc) {
+      FEK_CI(Q, qc);
+      if (key == NO_ERROR) {
+        R J[3][3];
+        point_jacobian<ET, Q>(X, J);
+        const int k = classify(det_ref(J), tol);
+        if (k) key = make_error_key(e_abs, Q, k);
+      }
+    });
+    return key;
+  }
+}
+
+template <typename R, int ET, int GEO>
+__global__ void __launch_bounds__(256) classify_kernel(const void *geometry, long long n, long long base,
+                                                       int lane_width, unsigned long long *error_key) {
+  constexpr int DS = 3 * Shape<ET>::NV;
+  const R *g = static_cast<const R *>(geometry);
+  unsigned long long best = NO_ERROR;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    R X[DS];
+    const long long blk = e / lane_width, lane = e % lane_width;
+#pragma unroll
+    for (int d = 0; d < DS; ++d) X[d] = g[blk * lane_width * DS + d * lane_width + lane];
+    const unsigned long long key = classify_exact<R, ET, GEO>(X, base + e);
+    best = key < best ? key : best;
+  }
+  if (best != NO_ERROR) atomicMin(error_key, best);
 }
 
 template <typename R, int ET>

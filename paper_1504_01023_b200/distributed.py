@@ -10,9 +10,13 @@ and the kernel's block/point/element error ordering is global.
 Collectives (NCCL over NVLink; gloo in CPU tests) run only AFTER the timed
 region, on a few bytes:
 
-* ``all_reduce(SUM)`` of the per-rank verification sums: the fp64 sums
-  (sum A, sum b, sum |A|, sum |b|) and the uint64 bit-pattern sums, which are
-  exactly additive, so the reduced value is bitwise the single-GPU value;
+* ``all_reduce(SUM)`` of the per-rank verification sums: the uint64
+  bit-pattern sums are exactly additive (wrapping integer sums), so their
+  reduced value is bitwise the single-GPU value; the fp64 sums (sum A, sum b,
+  sum |A|, sum |b|) match it only to rounding (fp64 addition is not
+  associative and the per-rank partition differs from ``fek_checksum``'s
+  592-block split), so verification gates on the bit-pattern sums and the
+  error key;
 * ``all_reduce(MIN)`` of the error key (first bad element over all ranks).
 """
 

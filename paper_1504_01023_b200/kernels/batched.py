@@ -11,9 +11,14 @@ same result type, same errors:
   H2D -> kernel -> D2H on three CUDA streams) and come back as numpy arrays,
   so a reference caller sees no difference; device batches stay on the GPU
   (``fek_integrate`` on the current torch stream) and return torch tensors.
-* ``workers`` is accepted for signature compatibility; the GPU decides the
-  parallel decomposition, and results are bitwise independent of it (as the
-  reference promises for its thread count, ``batched.py:10-13``).
+* ``workers`` does not change the launch (the GPU decides the parallel
+  decomposition; results are bitwise independent of it, as the reference
+  promises for its thread count, ``batched.py:10-13``).  It does change which
+  error is reported, exactly as in the reference: with ``workers > 1`` the batch
+  is split ``np.linspace(0, n, workers+1)``, each range applies the first-error
+  rule with 8192-element blocks counted from its own start, and the error with
+  the smallest element index wins (``batched.py:569-599``).  The GPU replays
+  that on the (rare) error path with one exact classification pass per range.
 * A degenerate/inverted element raises ``DegenerateElement`` /
   ``InvertedElement`` with the reference's element/point indices and message
   text; there is no partial result (``batched.py:544-547``).
@@ -31,7 +36,8 @@ import numpy as np
 
 from .. import _native, hostmem
 from ..errors import DegenerateElement, InvertedElement, NativeLibraryError, ShapeMismatch
-from ..layout import ELEMENT_MAJOR, BatchLayout, ElementBatch, LayoutKind, coerce_layout, flat_length, pack_rows
+from ..layout import (ELEMENT_MAJOR, BatchLayout, ElementBatch, LayoutKind, coerce_layout, flat_length, pack_rows,
+                      unpack_rows)
 from ..problems import (ElementMatrix, KernelDescriptor, ProblemClass, coerce_descriptor, coerce_element,
                         coerce_problem)
 from ..refelem import ElementType
@@ -344,13 +350,44 @@ _KIND_TEXT = {
 }
 
 
-def _raise_geometry(key: int, detail) -> None:
-    element, point, kind = _native.decode_error(key)
+def _raise_geometry(key, detail) -> None:
+    """Raise the reference's exception for an error key, or an (element, point, kind) triple."""
+    element, point, kind = _native.decode_error(key) if isinstance(key, int) else key
     if kind == _native.KIND_PIPELINE_TIMEOUT:
         raise NativeLibraryError("integration kernel pipeline timed out (internal error)")
     det, tol = detail(element, point)
     exc = DegenerateElement if kind == _native.KIND_DEGENERATE else InvertedElement
     raise exc(_KIND_TEXT[kind](det, tol), element, point)
+
+
+def _worker_rule_error(desc: KernelDescriptor, geometry_rows, dtype_code: int, n: int, workers: int,
+                       base_index: int, stream: int):
+    """First error under the reference's ``workers > 1`` rule (``batched.py:569-599``).
+
+    ``geometry_rows``: element-major (n, DS) CUDA tensor.  Each worker range
+    [lo, hi) of ``np.linspace(0, n, workers + 1)`` is classified exactly
+    (``fek_classify``) with its own block origin (``_run_range`` counts 8192-element
+    blocks from ``lo``); the worker error with the smallest element index wins.
+    Returns (element, point, kind) or None.
+    """
+    import torch
+
+    lib = _native.load()
+    bounds = np.linspace(0, n, workers + 1).astype(int)
+    keys = torch.full((workers,), -1, dtype=torch.int64, device=geometry_rows.device)
+    for w, (lo, hi) in enumerate(zip(bounds[:-1], bounds[1:])):
+        if hi <= lo:
+            continue
+        d = _desc_struct(desc, ELEMENT_MAJOR, int(hi - lo), 0, dtype_code, geometry_rows[int(lo)].data_ptr(), 0, 0,
+                         0, keys[w].data_ptr())
+        _native.check(lib.fek_classify(ctypes.byref(d), stream), "fek_classify")
+    found = []
+    for w, key in enumerate(keys.tolist()):
+        key &= _native.NO_ERROR
+        if key != _native.NO_ERROR:
+            e, q, k = _native.decode_error(key)
+            found.append((int(bounds[w]) + e + base_index, q, k))
+    return min(found, key=lambda t: t[0]) if found else None
 
 
 def _device_error_detail(dd: _native.BatchDesc, local: int, point, stream) -> tuple[float, float]:
@@ -399,8 +436,33 @@ def _tile_queue(dev, stream: int):
     return q
 
 
+def _check_out(out, batch: DeviceBatch, ns: int, packed: bool):
+    """Validate caller-supplied outputs before their pointers reach the kernel."""
+    import torch
+
+    if packed:
+        raise ValueError("out= cannot be combined with packed=True (the packed array is allocated here)")
+    if not isinstance(out, (tuple, list)) or len(out) != 2:
+        raise TypeError("out must be a pair (stiffness, load) of CUDA tensors")
+    n = batch.n_elements
+    for name, t, shape in (("stiffness", out[0], (n, ns, ns)), ("load", out[1], (n, ns))):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise TypeError(f"out {name} must be a CUDA tensor")
+        if t.device != batch.geometry_data.device:
+            raise ValueError(f"out {name} is on {t.device}, the batch on {batch.geometry_data.device}")
+        if t.dtype != batch.dtype:
+            raise TypeError(f"out {name} is {t.dtype}, the batch {batch.dtype}")
+        if tuple(t.shape) != shape:
+            raise ValueError(f"out {name} must have shape {shape}, got {tuple(t.shape)}")
+        if not t.is_contiguous():
+            raise ValueError(f"out {name} must be contiguous")
+        if n and t.data_ptr() % 16:
+            raise ValueError(f"out {name} storage must be 16-byte aligned")
+    return out[0], out[1]
+
+
 def _integrate_device(desc: KernelDescriptor, batch: DeviceBatch, out_layout, check: bool, base_index: int,
-                      out=None, packed: bool = False) -> BatchResult:
+                      out=None, packed: bool = False, workers: int = 1) -> BatchResult:
     import torch
 
     lib = _native.load()
@@ -410,6 +472,8 @@ def _integrate_device(desc: KernelDescriptor, batch: DeviceBatch, out_layout, ch
     olayout = coerce_layout(out_layout)
     flat = None
     if packed:
+        if out is not None:
+            _check_out(out, batch, ns, packed)
         flat = torch.empty(flat_length(n, ns * ns + ns, olayout), dtype=batch.dtype, device=dev)
         A, b = _packed_views(flat, n, ns, olayout)
         ptr_a, ptr_b = flat.data_ptr(), 0
@@ -418,7 +482,7 @@ def _integrate_device(desc: KernelDescriptor, batch: DeviceBatch, out_layout, ch
             A = torch.empty((n, ns, ns), dtype=batch.dtype, device=dev)
             b = torch.empty((n, ns), dtype=batch.dtype, device=dev)
         else:
-            A, b = out
+            A, b = _check_out(out, batch, ns, packed)
         ptr_a, ptr_b = A.data_ptr(), b.data_ptr()
     err = torch.full((1,), -1, dtype=torch.int64, device=dev)
     dd = _desc_struct(desc, batch.layout, n, base_index, dtype_code, batch.geometry_data.data_ptr(),
@@ -441,10 +505,33 @@ def _integrate_device(desc: KernelDescriptor, batch: DeviceBatch, out_layout, ch
         result.error_word = err
         result._queue = queue
         if check:
-            key = int(err.item()) & _native.NO_ERROR
+            key = resolve_error_key(dd, err, stream)
             if key != _native.NO_ERROR:
-                _raise_geometry(key, lambda e, q: _device_error_detail(dd, e - base_index, q, stream))
+                detail = lambda e, q: _device_error_detail(dd, e - base_index, q, stream)  # noqa: E731
+                if workers > 1:
+                    rows = batch if batch.layout.block == 1 else batch.convert(ELEMENT_MAJOR)
+                    geo = rows.geometry_data.view(n, desc.element.geometry_size)
+                    key = _worker_rule_error(desc, geo, dtype_code, n, workers, base_index, stream)
+                _raise_geometry(key, detail)
     return result
+
+
+def resolve_error_key(dd: _native.BatchDesc, err, stream: int) -> int:
+    """The reference's first-error key from a launch's error word (synchronises).
+
+    The kernels decide geometry classes on their own FMA det against 16x the
+    tolerance and report ``KIND_NEAR`` for anything closer (never on a valid
+    mesh); the exact pass ``fek_classify`` then re-derives the key with the
+    reference's rounding (``batched.py:151-177``).
+    """
+    key = int(err.item()) & _native.NO_ERROR
+    if key != _native.NO_ERROR and (key & 127) == _native.KIND_NEAR:
+        err.fill_(-1)
+        d = _native.BatchDesc.from_buffer_copy(dd)
+        d.error_key = err.data_ptr()
+        _native.check(_native.load().fek_classify(ctypes.byref(d), stream), "fek_classify")
+        key = int(err.item()) & _native.NO_ERROR
+    return key
 
 
 # ---------------------------------------------------------------------------
@@ -479,7 +566,8 @@ def _aligned_f64(a) -> np.ndarray:
     return a
 
 
-def _integrate_host(desc: KernelDescriptor, batch, out_layout, base_index: int, packed: bool = False) -> BatchResult:
+def _integrate_host(desc: KernelDescriptor, batch, out_layout, base_index: int, packed: bool = False,
+                    workers: int = 1) -> BatchResult:
     import torch
 
     if not torch.cuda.is_available():
@@ -527,7 +615,12 @@ def _integrate_host(desc: KernelDescriptor, batch, out_layout, base_index: int, 
             d1 = _desc_struct(desc, ELEMENT_MAJOR, 1, element, 0, g.data_ptr(), 0, 0, 0, 0)
             return _device_error_detail(d1, 0, point, cur.cuda_stream)
 
-        _raise_geometry(key.value, detail)
+        found = key.value
+        if workers > 1:
+            rows = unpack_rows(geo, n, desc.element.geometry_size, layout)
+            g = torch.from_numpy(np.ascontiguousarray(rows)).to(device)
+            found = _worker_rule_error(desc, g, _native.DTYPE["float64"], n, workers, base_index, cur.cuda_stream)
+        _raise_geometry(found, detail)
     _native.check(status, "fek_integrate_host")
     return BatchResult(desc, n, A, b, _traffic(desc, n), olayout, flat)
 
@@ -550,13 +643,15 @@ def integrate_batch(desc, batch, out_layout: BatchLayout = ELEMENT_MAJOR, worker
     """
     desc = coerce_descriptor(desc)
     _check_match(desc, batch)
-    if int(workers) < 1:
-        workers = 1
+    workers = max(1, min(int(workers), int(batch.n_elements)))  # batched.py:569
     if isinstance(batch, DeviceBatch):
-        return _integrate_device(desc, batch, out_layout, check, base_index, out, packed)
+        return _integrate_device(desc, batch, out_layout, check, base_index, out, packed, workers)
     if _is_torch(getattr(batch, "geometry_data", None)):
         raise TypeError("batches of torch tensors must be wrapped in DeviceBatch")
-    return _integrate_host(desc, batch, out_layout, base_index, packed)
+    if out is not None:
+        raise TypeError("out= is for device batches (host batches return numpy results)")
+    return _integrate_host(desc, batch, out_layout, base_index, packed, workers)
+
 
 
 def launch_config(desc, layout: BatchLayout, n: int, dtype: str = "float64") -> dict:

@@ -200,6 +200,42 @@ def error_cases():
         fh.write("\n".join(messages) + "\n")
 
 
+def workers_rule_rows(good, partly, n=20000, plant=((16000, "partly"), (16500, "inverted"))):
+    """Shifted reference prisms with failing elements planted at given indices."""
+    rows = np.tile(good.reshape(-1), (n, 1))
+    rows[:, 0::3] += 1e-3 * (np.arange(n) % 1000)[:, None]
+    for e, what in plant:
+        rows[e] = (partly if what == "partly" else -good).reshape(-1)
+    return rows
+
+
+def workers_cases():
+    """The workers > 1 first-error rule (batched.py:569-599) on a formula batch.
+
+    partly-inverted prism at 16000 (fails from q = 3 on), fully inverted one at 16500 (q = 0):
+    with one worker both sit in block [8192, 16384) / [16384, ...) and 16000 is reported;
+    with two workers the second range's first block [10000, 18192) holds both, and its
+    smallest-q rule reports 16500.
+    """
+    good = PRISM.reference_vertices.copy()
+    partly = good.copy()
+    partly[5, 2] = -3.0
+    rows = workers_rule_rows(good, partly)
+    out = {"prism_partly_inverted": partly}
+    for problem in (POISSON, CONVDIFF):
+        batch = ElementBatch.from_arrays(PRISM, problem, rows, np.zeros((rows.shape[0],
+                                                                         problem.coefficient_size(PRISM))))
+        for desc in case_descriptors(PRISM, problem):
+            for workers in (1, 2, 3, 7):
+                try:
+                    integrate_batch(desc, batch, workers=workers)
+                    raise AssertionError("expected a geometry error")
+                except GeometryError as err:
+                    kind = 1 if type(err).__name__ == "DegenerateElement" else 2
+                    out[f"w{workers}__{desc.short_name()}"] = np.array([kind, err.element_index, err.point_index])
+    _save("workers.npz", **out)
+
+
 def unit_elements():
     """Analytic goldens of test_kernels.py:55-85 / test_acceptance.py:169-196."""
     out = {}
@@ -214,6 +250,164 @@ def unit_elements():
                 out[f"A_{desc.short_name()}"] = res.stiffness[0]
                 out[f"b_{desc.short_name()}"] = res.load[0]
     _save("unit_elements.npz", **out)
+
+
+# ---------------------------------------------------------------------------
+# classification at the tolerance boundary (batched.py:136-177)
+# ---------------------------------------------------------------------------
+
+def _fma(a, b, c):
+    """IEEE fma, emulated exactly (float(Fraction) rounds to nearest even)."""
+    from fractions import Fraction
+    return float(Fraction(a) * Fraction(b) + Fraction(c))
+
+
+def _fused_det(J):
+    """det J as the round-1 kernels formed it (invert3 / prism_ref::adjugate: FMA cofactors)."""
+    (a, b, c), (d, e, f), (g, h, i) = J
+    k00 = _fma(e, i, -(f * h))
+    k01 = _fma(f, g, -(d * i))
+    k02 = _fma(d, h, -(e * g))
+    return _fma(a, k00, _fma(b, k01, c * k02))
+
+
+def _cube_cr(s):
+    from fractions import Fraction
+    return float(Fraction(s) ** 3)
+
+
+def _ref_point_dets(rows, et):
+    """Per-point (det, tol) lanes with the reference's own batched helpers."""
+    from feklab.geometry import DEGENERACY_REL_TOL
+    from feklab.kernels import batched as B
+
+    cols = B._columns(rows)
+    nv = et.n_vertices
+    scale = B._bbox_scale(cols, nv)
+    tol = DEGENERACY_REL_TOL * scale ** 3
+    _, table = reference_element(et)
+    dets, jacs = [], []
+    for q in range(et.n_quad):
+        ld = table.local_derivatives[q]
+        dx = [[B._axpy_fixed([ld[v, k] for v in range(nv)], [cols[v * 3 + i] for v in range(nv)])
+               for k in range(3)] for i in range(3)]
+        _, det = B._adjugate(dx)
+        dets.append(det)
+        jacs.append(np.array([[dx[i][k] for k in range(3)] for i in range(3)]))  # (3, 3, n)
+    return np.array(dets), tol, scale, jacs
+
+
+def _classes(dets, tol):
+    """Reference class per point: 1 degenerate, 2 inverted, 0 fine (batched.py:166-177)."""
+    deg = np.abs(dets) <= tol
+    inv = (dets < 0) & ~deg
+    return np.where(deg, 1, np.where(inv, 2, 0))
+
+
+def _boundary_candidates(et, rng, n):
+    """Nearly flat elements whose |det J| lies at the degeneracy bound, two regimes.
+
+    "ulp": one tet vertex (prism: the top face) within ~1e-14 of the rest, so det J is formed
+    from tiny columns and the element walks across tol in sub-ulp steps of det; "flat": O(1)
+    coordinates with det within a few percent of tol, where the reference's unfused det and an
+    FMA det differ by ~1% of tol.
+    """
+    nv = et.n_vertices
+    rows = np.empty((n, 3 * nv))
+    for r in range(n):
+        base = rng.uniform(-1, 1, (3, 3))
+        base[0] = 0.0
+        nrm = np.cross(base[1] - base[0], base[2] - base[0])
+        diag = np.linalg.norm(base.max(0) - base.min(0))
+        tol = 1e-14 * diag ** 3
+        sign = 1.0 if r % 4 else -1.0
+        regime = "ulp" if r % 2 == 0 else "flat"
+        target = sign * tol * (1.0 + (rng.uniform(-4, 4) * 2.0 ** -52 if regime == "ulp" else rng.uniform(-1e-3, 1e-3)))
+        if et is TET:
+            if regime == "ulp":
+                ab = rng.uniform(-1, 1, 2) * 1e-14 * diag
+            else:
+                ab = rng.uniform(0.2, 0.4, 2)
+            # det(v1 - v0, v2 - v0, v3 - v0) = nrm . (v3 - v0) for v3 = v0 + a e1 + b e2 + t nrm
+            t = target / float(nrm @ nrm)
+            v3 = base[0] + ab[0] * (base[1] - base[0]) + ab[1] * (base[2] - base[0]) + t * nrm
+            rows[r] = np.concatenate([base.reshape(-1), v3])
+        else:
+            # bottom triangle `base`, top = bottom + shear + h * normal: det J ~ area * h at every
+            # point; "flat" shears the top face in-plane by O(1), so det J is a cancellation of
+            # O(1) products, "ulp" keeps the zeta column tiny
+            area2 = float(np.linalg.norm(nrm))
+            shear = np.zeros(3)
+            if regime == "flat":
+                shear = rng.uniform(-0.5, 0.5) * (base[1] - base[0]) + rng.uniform(-0.5, 0.5) * (base[2] - base[0])
+            both = np.concatenate([base, base + shear])
+            tol = 1e-14 * np.linalg.norm(both.max(0) - both.min(0)) ** 3
+            target = sign * tol * (1.0 + rng.uniform(-1e-3, 1e-3))
+            off = rng.uniform(1 - 2e-4, 1 + 2e-4, 3)
+            h = target / (area2 * 0.5) * 2.0
+            lift = shear + np.outer(off * h, nrm / area2) / 2.0
+            rows[r] = np.concatenate([base.reshape(-1), (base + lift).reshape(-1)])
+    return rows
+
+
+def boundary_cases(per_type=48):
+    """Elements at |det J| ~ tol: the reference's classification, to the ulp.
+
+    Kept: elements whose bounding-box cube `scale**3` is the same under numpy's pow, math.pow
+    and the correctly rounded cube (numpy's AVX-512 pow is not correctly rounded on ~5% of
+    scales, so for the others the reference's own answer depends on the host ISA), preferring
+    ones the round-1 kernels (FMA det, (s*s)*s tol) classified differently from the reference.
+    Each fixture is a 3-element batch [valid, boundary, valid]; the reference's integrate_batch
+    result (error kind / element / point / message, or none) is stored for every descriptor.
+    """
+    import math
+
+    rng = np.random.default_rng(SEED + 11)
+    out, messages, stats = {}, [], {}
+    for et in (TET, PRISM):
+        rows = _boundary_candidates(et, rng, 4000)
+        dets, tol, scale, jacs = _ref_point_dets(rows, et)
+        keep_diff, keep_same = [], []
+        for e in range(rows.shape[0]):
+            s = float(scale[e])
+            if not (s ** 3 == math.pow(s, 3) == _cube_cr(s) == float(np.power(np.array([s]), 3)[0])):
+                continue
+            ref = _classes(dets[:, e], tol[e])
+            near = np.abs(np.abs(dets[:, e]) / tol[e] - 1.0) < 0.05
+            if not near.any():
+                continue
+            old_tol = 1e-14 * ((s * s) * s)
+            old = _classes(np.array([_fused_det(jacs[q][:, :, e]) for q in range(et.n_quad)]), old_tol)
+            first = lambda c: (int(np.flatnonzero(c)[0]), int(c[np.flatnonzero(c)[0]])) if c.any() else None
+            (keep_diff if first(old) != first(ref) else keep_same).append(e)
+        stats[et.value] = (len(keep_diff), len(keep_same))
+        chosen = keep_diff[: per_type // 2] + keep_same[: per_type - min(len(keep_diff), per_type // 2)]
+        rows_out = []
+        for j, e in enumerate(chosen):
+            els = [(random_geometry(et, rng), None), (ElementGeometry(et, rows[e].reshape(-1, 3)), None),
+                   (random_geometry(et, rng), None)]
+            g3 = np.stack([g.coords.reshape(-1) for g, _ in els])
+            rows_out.append(g3)
+            for problem in (POISSON, CONVDIFF):
+                cof = np.ones((3, problem.coefficient_size(et)))
+                batch = ElementBatch.from_arrays(et, problem, g3, cof)
+                for desc in case_descriptors(et, problem):
+                    name = f"{et.value}_{j}__{desc.short_name()}"
+                    try:
+                        integrate_batch(desc, batch)
+                        out[name] = np.array([0, -1, -1])
+                        messages.append(f"{name}\t")
+                    except GeometryError as err:
+                        kind = 1 if type(err).__name__ == "DegenerateElement" else 2
+                        out[name] = np.array([kind, err.element_index,
+                                              -1 if err.point_index is None else err.point_index])
+                        messages.append(f"{name}\t{err}")
+        out[f"{et.value}_geometry"] = np.stack(rows_out)
+        out[f"{et.value}_round1_misclassified"] = np.array([min(len(keep_diff), per_type // 2)])
+    _save("boundary.npz", **out)
+    with open(os.path.join(HERE, "boundary_messages.tsv"), "w") as fh:
+        fh.write("\n".join(messages) + "\n")
+    print("boundary candidates (round-1 kernel differs, agrees):", stats, file=sys.stderr)
 
 
 SLICE = 1024  # sampled elements per benchmark configuration
@@ -261,10 +455,16 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["bench"]:
         bench_slices()
         sys.exit(0)
+    if sys.argv[1:] == ["boundary"]:
+        boundary_cases()
+        workers_cases()
+        sys.exit(0)
     refelem()
     corpora()
     twisted_prisms()
     meshes()
     error_cases()
+    boundary_cases()
+    workers_cases()
     unit_elements()
     bench_slices()

@@ -98,3 +98,37 @@ def test_oracle_first_error_rule():
             assert (kind, err.value.element_index, point) == tuple(want), (name, v, p)
             checked += 1
     assert checked >= 20
+
+
+def boundary_fixtures():
+    """(et, j, geometry rows, {descriptor short name: (kind, element, point)}) of boundary.npz."""
+    z = golden("boundary.npz")
+    for et in ("tet", "prism"):
+        geo = z[f"{et}_geometry"]
+        for j in range(geo.shape[0]):
+            want = {k.split("__")[1]: tuple(int(x) for x in z[k]) for k in z.files if k.startswith(f"{et}_{j}__")}
+            yield et, j, geo[j], want
+
+
+def test_oracle_classification_at_the_tolerance_boundary():
+    """|det J| within ~1e-3 (and within ulps) of 1e-14 diag^3: bitwise the reference's verdicts.
+
+    The fixtures hold elements whose bounding-box cube is host-independent (make_golden.py
+    boundary_cases), so the oracle's own numpy `scale**3` reproduces the reference's here too.
+    """
+    checked = errors = 0
+    for et, j, geo, want in boundary_fixtures():
+        for name, code in want.items():
+            v, p = name.split("_")[:2]
+            pb = name.split("_")[-1]
+            cof = np.ones((3, (4 if et == "tet" else 6) if pb == "poisson" else 20))
+            try:
+                O.integrate(v, p, pb, et, geo, cof)
+                got = (0, -1, -1)
+            except O.OracleGeometryError as err:
+                got = (1 if err.kind == "degenerate" else 2, err.element_index,
+                       -1 if err.point_index is None else err.point_index)
+                errors += 1
+            assert got == code, (et, j, name)
+            checked += 1
+    assert checked >= 800 and errors >= 400
