@@ -57,3 +57,20 @@ class CounterMismatch(FeklabError):
 
 class NativeLibraryError(FeklabError, RuntimeError):
     """libfek.so is unavailable or a CUDA call behind the C-ABI failed."""
+
+
+BOUNDARY_TYPES = ("GeometryError", "DegenerateElement", "InvertedElement", "ShapeMismatch")
+
+
+def bind_exception_types(namespace) -> None:
+    """Raise a host package's own exception classes across the boundary.
+
+    ``integrate_batch`` / ``integrate_element`` / the geometry helpers look the
+    classes up here at raise time, so after ``bind_exception_types(feklab.errors)``
+    a feklab caller catching ``feklab.errors.DegenerateElement`` catches the
+    drop-in's errors unchanged.  The classes must take
+    ``(message, element_index, point_index)`` as the reference's do (``errors.py:8-19``).
+    """
+    g = globals()
+    for name in BOUNDARY_TYPES:
+        g[name] = getattr(namespace, name)

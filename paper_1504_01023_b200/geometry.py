@@ -24,7 +24,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .errors import DegenerateElement, InvertedElement
+from . import errors as _errors
 from .refelem import ElementType, QuadratureRule, ShapeFunctionTable
 
 DEGENERACY_REL_TOL = 1e-14
@@ -85,9 +85,9 @@ def _device_jacobian(geom: ElementGeometry, point: int) -> tuple[np.ndarray, np.
 def _check(det: float, tol: float, element_index, point_index) -> None:
     """Degenerate first, then inverted (``geometry.py:81-91``)."""
     if abs(det) <= tol:
-        raise DegenerateElement(f"|det J| = {abs(det):.3e} <= {tol:.3e}", element_index, point_index)
+        raise _errors.DegenerateElement(f"|det J| = {abs(det):.3e} <= {tol:.3e}", element_index, point_index)
     if det < 0.0:
-        raise InvertedElement(f"det J = {det:.3e} < 0", element_index, point_index)
+        raise _errors.InvertedElement(f"det J = {det:.3e} < 0", element_index, point_index)
 
 
 def jacobian_affine(geom: ElementGeometry, rule: QuadratureRule, element_index=None) -> JacobianData:

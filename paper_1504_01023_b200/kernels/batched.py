@@ -35,7 +35,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .. import _native, hostmem
-from ..errors import DegenerateElement, InvertedElement, NativeLibraryError, ShapeMismatch
+from .. import errors as _errors
+from ..errors import NativeLibraryError
 from ..layout import (ELEMENT_MAJOR, BatchLayout, ElementBatch, LayoutKind, coerce_layout, flat_length, pack_rows,
                       unpack_rows)
 from ..problems import (ElementMatrix, KernelDescriptor, ProblemClass, coerce_descriptor, coerce_element,
@@ -340,7 +341,7 @@ def _traffic(desc: KernelDescriptor, n: int) -> TrafficCounters:
 def _check_match(desc: KernelDescriptor, batch) -> None:
     etype, problem = coerce_element(batch.element_type), coerce_problem(batch.problem)
     if etype is not desc.element or problem is not desc.problem:
-        raise ShapeMismatch(f"descriptor ({desc.element.value}, {desc.problem.value}) does not match "
+        raise _errors.ShapeMismatch(f"descriptor ({desc.element.value}, {desc.problem.value}) does not match "
                             f"batch ({etype.value}, {problem.value})")
 
 
@@ -356,7 +357,7 @@ def _raise_geometry(key, detail) -> None:
     if kind == _native.KIND_PIPELINE_TIMEOUT:
         raise NativeLibraryError("integration kernel pipeline timed out (internal error)")
     det, tol = detail(element, point)
-    exc = DegenerateElement if kind == _native.KIND_DEGENERATE else InvertedElement
+    exc = _errors.DegenerateElement if kind == _native.KIND_DEGENERATE else _errors.InvertedElement
     raise exc(_KIND_TEXT[kind](det, tol), element, point)
 
 

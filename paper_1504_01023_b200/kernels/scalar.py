@@ -9,7 +9,7 @@ so a batch of identical elements is bitwise equal to ``integrate_element``
 
 from __future__ import annotations
 
-from ..errors import ShapeMismatch
+from .. import errors as _errors
 from ..layout import build_batch
 from ..problems import ElementMatrix, ProblemClass, coerce_descriptor, coerce_element, coerce_problem
 from .batched import integrate_batch
@@ -18,9 +18,9 @@ from .batched import integrate_batch
 def integrate_element(desc, geom, coeff) -> ElementMatrix:
     desc = coerce_descriptor(desc)
     if coerce_element(geom.element) is not desc.element:
-        raise ShapeMismatch(f"descriptor expects {desc.element.value}, geometry is {geom.element.value}")
+        raise _errors.ShapeMismatch(f"descriptor expects {desc.element.value}, geometry is {geom.element.value}")
     if coerce_problem(coeff.problem) is not desc.problem:
-        raise ShapeMismatch(f"descriptor expects {desc.problem.value}, coefficients are {coeff.problem.value}")
+        raise _errors.ShapeMismatch(f"descriptor expects {desc.problem.value}, coefficients are {coeff.problem.value}")
     if desc.problem is ProblemClass.POISSON and len(coeff.d0) != desc.element.n_quad:
-        raise ShapeMismatch(f"expected {desc.element.n_quad} right-hand-side values, got {len(coeff.d0)}")
+        raise _errors.ShapeMismatch(f"expected {desc.element.n_quad} right-hand-side values, got {len(coeff.d0)}")
     return integrate_batch(desc, build_batch([(geom, coeff)])).element_matrix(0)
