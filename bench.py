@@ -1,31 +1,37 @@
 #!/usr/bin/env python
 """bench.py -- elements integrated per second on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C5]
     torchrun --nproc-per-node N bench.py --gpus N ...           (N > 1; plain `python bench.py
                                                                 --gpus N` starts torchrun itself)
 
-Headline workload (N=1, BASELINE.json configs[1] -> SURVEY config C2):
-generalized convection-diffusion-reaction on 4,088,832 linear tetrahedra
-(88^3 Kuhn cells), per-element coefficients, fp64, natural QSS geo_linear
-descriptor.  One step = one ``fek_integrate`` launch over the whole batch.
-Scaling is weak: every rank integrates its own C2-sized range of a
-(rank-seeded) mesh, base_index = rank*n, no collective on the hot path.
+Headline workload (BASELINE.json configs[4], the metric's "at 1/2/4/8 B200" configuration and
+the largest that fits one GPU; SURVEY config C5): the 64,156,250-element mixed tetra/prism
+convection-diffusion-reaction mesh -- 175^3 x 6 Kuhn tets + 4000^2 x 2 jittered (non-affine)
+prisms, per-element coefficients, fp64 -- as the reference holds it: two homogeneous batches
+(layout.py:185-190), each split by contiguous element range across the N GPUs
+(batched.py:569-573's worker split, rounded to 128-element tiles; base_index = range start).
+One step = this rank's tet launch + prism launch (two ``fek_integrate`` calls).  Scaling is
+STRONG: the total work is fixed, value = 64,156,250 / max-over-ranks step time.
 
 Printed JSON (rank 0, one line):
-  value      whole-job elements/s, inputs already in HBM (device events, max
-             over ranks; 1.7 GB of traffic per step >> 126 MB L2);
-  e2e        same metric through the public API ``integrate_batch(desc,
-             host_batch)`` with page-locked host buffers: H2D + kernel + D2H
-             inside the timed region;
-  roofline   of the integration kernel (algorithmic bytes / launch time vs the
-             measured HBM copy peak);
-  cpu_baseline  the reference algorithm (oracle port) on all host cores;
-  cases      C1/C3/C4 (fp64, C4 also fp32) kernel timings + rooflines;
-  parity     GPU vs CPU oracle on the full C2 batch and on case samples.
+  value      whole-job elements/s, inputs already in HBM (generated there by the device mesh
+             generator, bit-identical to the reference's), K steps replayed as one CUDA graph,
+             CUDA events on its stream, max over ranks; 34 GB of traffic per step >> 126 MB L2;
+  e2e        the same metric through the public API -- ``integrate_batch(desc, ElementBatch)``
+             on both host batches of this rank's shard, page-locked host arrays, H2D + kernel +
+             D2H inside the timed region, max over ranks; ``e2e.pageable`` the same call on plain
+             (pageable) numpy arrays, as a reference caller's ElementBatch holds them;
+  roofline   of the dominant kernel (prism ConvDiff: algorithmic bytes per launch / its average
+             launch time from CUDA events on its stream) + the step's concurrent roof;
+  cpu_baseline  the reference algorithm (bitwise numpy port) on all host cores, on a sample of
+             both batches, extrapolated to the C5 mix;
+  parity     GPU vs the port on that sample (bitwise-pinned restatement of the reference);
+  cases      C1-C4, C4 fp32, C2 packed: single-configuration kernel timings (N=1).
 
-``--impl reference`` times the reference's CPU algorithm (oracle port) on the
-same workload, on rank 0 only.
+``--impl reference`` times the STOCK reference (``baseline/_ref/feklab.integrate_batch``, its
+best ``workers`` count) on samples of both C5 batches, rank 0 only.
+``--config C1|C2|C3|C4`` runs the single-configuration weak-scaling mode instead.
 """
 
 from __future__ import annotations
@@ -44,6 +50,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "elements integrated/sec (fp64) at 1/2/4/8 B200; % of HBM/FP64 roofline"
 UNIT = "elements/s"
+C5_WORKLOAD = "C5: 64,156,250-element mixed tetra/prism CDR mesh (175^3x6 tets + 4000^2x2 jittered prisms), fp64"
 L2_BYTES = 126 * 2 ** 20
 
 
@@ -53,8 +60,8 @@ def parse(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--cases", default="C1,C3,C4,C4f32,C5,C2packed",
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--cases", default="C1,C2,C3,C4,C4f32,C2packed",
                     help="extra per-config kernel timings (N=1 only)")
     ap.add_argument("--no-cases", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -89,67 +96,101 @@ def _config_record(cfg, n_per_rank, world, desc, extra=None):
 # reference arm
 # ---------------------------------------------------------------------------
 
+C5_PARTS = ("C5T", "C5P")
+C5_TOTAL = 64_156_250
+REF_SAMPLE = 32_768  # elements per batch per reference step (4 blocks of 8192)
+
+
+def _stock_reference():
+    """The stock reference package from baseline/_ref (pip-installed from /root/reference), or None."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "feklab")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import feklab
+
+    if not os.path.abspath(feklab.__file__).startswith(ref):
+        raise RuntimeError(f"feklab imported from {feklab.__file__}, not baseline/_ref")
+    return feklab
+
+
 def run_reference(args) -> int:
-    from oracle.cpu_baseline import PortPool, cpu_cores
-    from paper_1504_01023_b200 import KernelDescriptor, mesh, natural_path
+    """The stock reference's integrate_batch on samples of the configuration, rank 0 only.
+
+    Each step integrates the first REF_SAMPLE elements of every batch of the workload (for C5:
+    both the tet and the prism batch) with ``feklab.integrate_batch`` -- the reference's own public
+    API and numpy code path, natural QSS descriptor, at the ``workers`` count (threads) that was
+    fastest in a warm-up sweep over {1, 2, 4, cores}; the reference's own bench sweeps workers the
+    same way (pkg/src/feklab/bench.py:23-33).  Inputs are rows [0, REF_SAMPLE) of the benchmark mesh
+    (mesh.config_window: the same elements the reference's generate_mesh makes).  ``value`` is the
+    configuration's element count over its extrapolated time: sum over batches of (batch elements x
+    measured seconds per element of its sample).
+    """
+    from oracle.cpu_baseline import cpu_cores
+    from paper_1504_01023_b200 import mesh
     from paper_1504_01023_b200.distributed import env_rank
-    from paper_1504_01023_b200.problems import Variant
 
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
+    feklab = _stock_reference()
+    if feklab is None:
+        print(json.dumps({"impl": "reference", "unavailable": "baseline/_ref not installed (run "
+                                                              "__graft_entry__.build() where /root/reference exists)"}))
+        return 0
+    from feklab.layout import ElementBatch as RefBatch
+    from feklab.problems import GeometryPath, KernelDescriptor, ProblemClass, Variant
+    from feklab.refelem import ElementType
+
     cores = cpu_cores()
-    procs = args.cpu_processes or cores["logical"] or 1
-    keys = ("C5T", "C5P") if args.config == "C5" else (args.config,)
-    sample_each = (1 << 19) // len(keys)
-    sec, sample = 0.0, 0
+    keys = C5_PARTS if args.config == "C5" else (args.config,)
+    work = []
     for key in keys:
         cfg = mesh.bench_configs()[key]
-        et, pb = cfg.spec.element_type, cfg.problem
-        desc = KernelDescriptor(Variant(args.variant), natural_path(et), pb, et)
-        # host rows of a contiguous sample window only (the reference generator
-        # is sequential; C5 is 64M elements): first `window` elements
-        window = min(cfg.spec.n_elements, 4 * sample_each)
-        if cfg.spec.n_elements <= (1 << 23):
-            geo, cof = mesh.config_rows(cfg)
-        else:
-            import torch
+        et = ElementType(cfg.spec.element_type.value)
+        pb = ProblemClass(cfg.problem.value)
+        path = GeometryPath.GEO_LINEAR if et is ElementType.TETRAHEDRON else GeometryPath.GEO_GENERIC
+        geo, cof = mesh.config_window(cfg, REF_SAMPLE)
+        work.append((cfg, KernelDescriptor(Variant(args.variant), path, pb, et), RefBatch.from_arrays(et, pb, geo, cof)))
 
-            g, c = mesh.device_config(cfg, 0, window) if torch.cuda.is_available() else (None, None)
-            if g is None:
-                geo, cof = mesh.config_rows(cfg)
-            else:
-                geo = g.cpu().numpy().reshape(window, -1)
-                cof = c.cpu().numpy().reshape(window, -1)
-        n = geo.shape[0]
-        part = min(n, sample_each)
-        times = []
-        with PortPool(desc.variant.value, desc.geometry_path.value, pb.value, et.value, geo, cof, procs) as pool:
-            warm_until = time.perf_counter() + 1.0  # >= 1 s: worker heaps, page tables, CPU clocks settle
-            done = 0
-            while done < max(args.warmup, 1) or time.perf_counter() < warm_until:
-                pool.run(0, part)
-                done += 1
-            for _ in range(args.steps):  # same window every step, as the reference's bench repeats its batch
-                times.append(pool.run(0, part))
-        sec += float(np.mean(times))
-        sample += part
-    cfg = mesh.bench_configs()[keys[0]]
-    desc = KernelDescriptor(Variant(args.variant), natural_path(cfg.spec.element_type), cfg.problem,
-                            cfg.spec.element_type)
-    n = sum(mesh.bench_configs()[k].spec.n_elements for k in keys)
-    value = sample / sec
+    def step(workers):
+        per = []
+        for cfg, desc, batch in work:
+            t0 = time.perf_counter()
+            feklab.integrate_batch(desc, batch, workers=workers)
+            per.append(time.perf_counter() - t0)
+        return per
+
+    sweep = {}
+    for w in sorted({1, 2, 4, cores["logical"] or 1}):
+        step(w)
+        sweep[w] = sum(step(w))
+    workers = min(sweep, key=sweep.get)
+    for _ in range(max(args.warmup, 1)):
+        step(workers)
+    times = np.array([step(workers) for _ in range(args.steps)])   # (steps, batches)
+    per_elem = times.mean(axis=0) / np.array([b.n_elements for *_, b in work])
+    n_total = sum(cfg.spec.n_elements for cfg, *_ in work)
+    t_full = float(sum(cfg.spec.n_elements * pe for (cfg, *_), pe in zip(work, per_elem)))
+    value = n_total / t_full
+    sample = " + ".join(f"{b.n_elements} {cfg.key}" for cfg, _, b in work)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference mesh generator, seeded coefficients)",
-        "config": _config_record(cfg, n, 1, desc, {"sample_elements_per_step": sample,
-                                                   "workload_parts": list(keys)}),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
-                         "sample": f"{sample} contiguous elements of {cfg.key} per step (oracle port of "
-                                   f"feklab integrate_batch, {procs} processes)", "host_cores": cores},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(times.sum(axis=1).mean() * 1e3),
+        "higher_is_better": True, "scaling": "strong" if args.config == "C5" else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic: rows [0, sample) of the benchmark meshes (reference element order "
+                                "and coefficient streams)",
+        "config": {"workload": (C5_WORKLOAD if args.config == "C5" else mesh.bench_configs()[args.config].text),
+                   "elements_total": n_total, "sample_elements_per_step": int(sum(b.n_elements for *_, b in work)),
+                   "workload_parts": list(keys)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference",
+                         "sample": f"{sample} elements per step through stock feklab.integrate_batch "
+                                   f"(baseline/_ref, workers={workers}), extrapolated to the full mix",
+                         "host_cores": cores, "workers_sweep_s_per_step": sweep,
+                         "seconds_per_element": {cfg.key: float(pe) for (cfg, *_), pe in zip(work, per_elem)}},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_package": os.path.dirname(feklab.__file__),
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -399,100 +440,342 @@ def c5_parts(world: int, rank: int):
     return parts
 
 
-def measure_c5(steps, warmup, world=1, rank=0, sampler=None, barrier=None):
-    """C5: 64M-element mixed CDR mesh = one tet batch + one prism batch, range-sharded.
+def load_profile_traffic(kernel_tag: str, n: int | None = None):
+    """DRAM bytes per launch of a kernel from the committed ncu summary (profiles/ncu_summary.json).
 
-    A step integrates this rank's shard of both batches.  Inputs are generated
-    in HBM by the device mesh generator.  Schedules timed:
-    * serial  -- tet launch then prism launch on one stream, the K steps
-      replayed as one CUDA graph (`serial_eager`: the same on an eager stream);
-    * overlap_eager -- the memory-bound tet launch capped at 1 CTA per SM on a
-      side stream with static tiles, the FP64-bound prism launch concurrently
-      on the main stream taking the remaining slots from the dynamic tile queue.
-    The record's headline is the fastest.
+    With ``n``: scaled from the captured launch's element count to n elements (the capture's
+    configuration is named in its report file, e.g. prof_C4_r01 -> C4).
     """
-    import torch
-
-    from paper_1504_01023_b200 import mesh
-    from paper_1504_01023_b200.kernels.counts import algorithmic_bytes, algorithmic_flops
-    from paper_1504_01023_b200.measure import flop_peak, hbm_peak
-
-    if sampler is None:
-        from paper_1504_01023_b200.measure import ClockSampler
-
-        sampler = ClockSampler(torch.cuda.current_device(), period=0.0005)
-    launchers, parts = [], c5_parts(world, rank)
-    for cfg, desc, lo, n in parts:
-        geo, cof = mesh.device_config(cfg, lo, n)
-        launchers.append((Launcher(desc, geo, cof, base_index=lo), desc, geo, cof))
-
-    def serial():
-        for L, *_ in launchers:
-            L()
-
-    serial.launchers = [L for L, *_ in launchers]
-
-    side = torch.cuda.Stream()
-    (LT, *_), (LP, *_) = launchers
-    overlap_tet = LT.clone(dynamic=False, ctas_per_sm=1, stream=side.cuda_stream)
-
-    def overlap():
-        cur = torch.cuda.current_stream()
-        side.wait_stream(cur)
-        overlap_tet()
-        LP()
-        cur.wait_stream(side)
-
-    modes = {"serial": time_graph([serial], steps, warmup, sampler, barrier) / steps,
-             "serial_eager": time_launches([serial], steps, warmup)[1] / steps,
-             "overlap_eager": time_launches([overlap], steps, warmup)[1] / steps}
-    if barrier is not None:  # multi-rank: every rank picks the same schedule (slowest rank per schedule)
-        import torch.distributed as dist
-
-        t = torch.tensor(list(modes.values()), dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        modes = dict(zip(modes, t.tolist()))
-    best = min(modes, key=modes.get)
-    if best != "serial" and sampler is not None:  # re-time the winner under the clock sampler
-        modes[best] = time_launches([serial if best == "serial_eager" else overlap], steps, warmup, sampler)[1] / steps
-    total_ms = modes[best] * steps
-    for L, *_ in launchers:
-        if L.error_key() != 0xFFFFFFFFFFFFFFFF:
-            raise RuntimeError(f"C5: unexpected geometry error key {L.error_key():#x}")
-    ms = total_ms / steps
-    n_local = sum(n for *_, n in parts)
-    hbm, _ = hbm_peak()
-    fp, _ = flop_peak(8)
-    by = sum(algorithmic_bytes(d.element, d.problem) * n for _, d, _, n in parts)
-    fl = sum(algorithmic_flops(d.element, d.problem) * n for _, d, _, n in parts)
-    t_roof = max(by / (hbm * 1e9), fl / (fp * 1e12))
-    serial = sum(max(algorithmic_bytes(d.element, d.problem) * n / (hbm * 1e9),
-                     algorithmic_flops(d.element, d.problem) * n / (fp * 1e12)) for _, d, _, n in parts)
-    parity = {}
-    for (L, desc, geo, cof), (cfg, *_) in zip(launchers, parts):
-        err, cnt = sample_parity(desc, geo, cof, L.A, L.b, count=4096)
-        parity[cfg.key] = {"max_rel_frobenius": err, "elements_checked": cnt, "pass": err <= 1e-12}
-    rec = {"workload": "C5: 64,156,250-element mixed CDR mesh (175^3x6 tets + 4000^2x2 jittered prisms)",
-           "elements_this_rank": n_local, "ms_per_step": ms, "value_this_rank": n_local / (ms / 1e3),
-           "schedule": best, "ms_per_step_by_schedule": modes, "clocks": sampler.summary(),
-           "roofline": {"bound": "concurrent max(sum bytes/HBM, sum flops/FP64)", "roof_ms": t_roof * 1e3,
-                        "frac": t_roof / (ms / 1e3), "serialized_by_type_roof_ms": serial * 1e3,
-                        "frac_of_serialized": serial / (ms / 1e3)},
-           "parity": parity}
-    del launchers
-    torch.cuda.empty_cache()
-    return rec
+    rec = load_profile_record(kernel_tag)
+    if not rec or rec.get("dram_bytes_per_launch") is None:
+        return None
+    if n is None:
+        return rec["dram_bytes_per_launch"]
+    per = rec.get("_per_element")
+    return None if per is None else per["dram_bytes"] * n
 
 
-def load_profile_traffic(kernel_tag: str):
-    """Per-launch dram bytes from the committed ncu summary, if present."""
+def load_profile_record(kernel_tag: str):
+    import re
+
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
-            data = json.load(fh)
-        return data.get(kernel_tag, {}).get("dram_bytes_per_launch")
+            rec = dict(json.load(fh).get(kernel_tag) or {})
     except Exception:
         return None
+    m = re.match(r"prof_(C\d[A-Z]?)", rec.get("report", ""))
+    if m and rec:
+        from paper_1504_01023_b200 import mesh
+
+        n = rec.get("elements") or mesh.bench_configs()[m.group(1)].spec.n_elements
+        rec["_per_element"] = {"dram_bytes": rec.get("dram_bytes_per_launch", 0) / n,
+                               "fp64_flops": rec.get("executed_fp64_flops", 0) / n, "elements_captured": n}
+    return rec
+
+
+# ---------------------------------------------------------------------------
+# C5 headline (strong scaling over element-range shards of both batches)
+# ---------------------------------------------------------------------------
+
+class Part:
+    """One rank's shard of one C5 batch: device inputs (generated in HBM) + a prepared launch."""
+
+    def __init__(self, cfg, desc, lo, n):
+        from paper_1504_01023_b200 import mesh
+
+        self.cfg, self.desc, self.lo, self.n = cfg, desc, lo, n
+        self.geo, self.cof = mesh.device_config(cfg, lo, n)
+        self.L = Launcher(desc, self.geo, self.cof, base_index=lo)
+
+
+def time_parts(parts, steps, warmup):
+    """Mean device ms of each part's launch: CUDA events on the launch stream around every launch
+    of `steps` serial steps (the per-kernel split of a step; the graph replay times the step)."""
+    import torch
+
+    for _ in range(warmup):
+        for p in parts:
+            p.L()
+    torch.cuda.synchronize()
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in parts]
+           for _ in range(steps)]
+    for k in range(steps):
+        for i, p in enumerate(parts):
+            evs[k][i][0].record()
+            p.L()
+            evs[k][i][1].record()
+    torch.cuda.synchronize()
+    return [float(np.mean([evs[k][i][0].elapsed_time(evs[k][i][1]) for k in range(steps)]))
+            for i in range(len(parts))]
+
+
+def c5_e2e(parts, steps, barrier=None, pageable=False):
+    """ms per step of the public API on host batches of this rank's shards (H2D + kernel + D2H).
+
+    Inputs are downloaded from HBM untimed.  pinned: ElementBatch.from_arrays (page-locked flat
+    arrays, as this package builds them); pageable: plain numpy arrays, as a reference caller's
+    ElementBatch holds them (layout.py:103-112).
+    """
+    import torch
+
+    from paper_1504_01023_b200 import ElementBatch, integrate_batch
+    from paper_1504_01023_b200.layout import ELEMENT_MAJOR
+
+    batches = []
+    for p in parts:
+        g = p.geo.view(p.n, -1).cpu().numpy()
+        c = p.cof.view(p.n, -1).cpu().numpy()
+        if pageable:
+            batches.append(ElementBatch(p.desc.element, p.desc.problem, p.n, ELEMENT_MAJOR, g.reshape(-1),
+                                        c.reshape(-1)))
+        else:
+            batches.append(ElementBatch.from_arrays(p.desc.element, p.desc.problem, g, c))
+            del g, c
+    res = [None] * len(parts)
+
+    def step():
+        for i, p in enumerate(parts):
+            res[i] = None   # the previous result's page-locked blocks go back to the caching allocator
+            res[i] = integrate_batch(p.desc, batches[i], base_index=p.lo)
+
+    step()
+    torch.cuda.synchronize()
+    if barrier is not None:
+        barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        step()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / steps
+    h2d = sum(b.geometry_data.nbytes + b.coefficient_data.nbytes for b in batches)
+    d2h = sum(r.stiffness.nbytes + r.load.nbytes for r in res)
+    m = min(p.n for p in parts)
+    k = min(m, 1 << 20)
+    same = all(np.array_equal(r.stiffness[:k], p.L.A[:k].cpu().numpy()) and
+               np.array_equal(r.load[:k], p.L.b[:k].cpu().numpy()) for r, p in zip(res, parts))
+    return ms, int(h2d), int(d2h), bool(same)
+
+
+def c5_cpu_baseline(parts, sample: int, procs: int):
+    """The bitwise numpy port on `procs` processes over the first `sample` elements of each part
+    (host rows downloaded from HBM), plus GPU-vs-port parity on exactly those elements."""
+    from oracle import numpy_oracle as O
+    from oracle.cpu_baseline import PortPool
+
+    per_elem, checked, err = {}, 0, 0.0
+    for p in parts:
+        m = min(sample, p.n)
+        geo = p.geo.view(p.n, -1)[:m].cpu().numpy()
+        cof = p.cof.view(p.n, -1)[:m].cpu().numpy()
+        d = p.desc
+        with PortPool(d.variant.value, d.geometry_path.value, d.problem.value, d.element.value, geo, cof,
+                      procs) as pool:
+            pool.run(0, m)  # warm: worker heaps, page tables, CPU clocks
+            sec = float(np.mean([pool.run(0, m) for _ in range(3)]))
+            errA = float(O.rel_frobenius(p.L.A[:m].cpu().numpy(), pool.A).max())
+            errb = float(O.rel_frobenius(p.L.b[:m].cpu().numpy(), pool.b).max())
+        per_elem[p.cfg.key] = sec / m
+        err = max(err, errA, errb)
+        checked += m
+    return per_elem, err, checked
+
+
+def c5_verify(parts) -> dict:
+    """After timing: MIN error key and SUM bit-pattern checksums of every rank's shards.
+
+    ``parts``: (descriptor, first element, count, batch key, Launcher) of this rank's shards.  The
+    bit-pattern sums weight each entry by its absolute index (base_index = shard start), so the
+    reduced sums equal a single launch's over the whole batch bit for bit; the MIN of the
+    order-preserving error keys is the globally first bad element (NCCL under torchrun, gloo in
+    tests/test_gpu_multirank.py).
+    """
+    from paper_1504_01023_b200.distributed import allreduce_error_key, allreduce_sums, device_checksum
+    from paper_1504_01023_b200.kernels.batched import BatchResult, _traffic
+
+    ver = {}
+    for desc, lo, n, key, L in parts:
+        key_all = allreduce_error_key(L.error_key())
+        res = BatchResult(desc, n, L.A, L.b, _traffic(desc, n))
+        f, u = allreduce_sums(*device_checksum(res, base_index=lo))
+        ver[key] = {"error_key_all_ranks": key_all, "sum_A": float(f[0]),
+                    "bitsum_A": int(u[0].item()) & 0xFFFFFFFFFFFFFFFF,
+                    "bitsum_b": int(u[1].item()) & 0xFFFFFFFFFFFFFFFF}
+    ver["collectives"] = "all_reduce(MIN error key, SUM bit-pattern sums) after timing"
+    return ver
+
+
+def run_c5(args) -> int:
+    """The headline: C5 strong-scaled over N GPUs (each rank generates and integrates its shards)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1504_01023_b200 import mesh
+    from paper_1504_01023_b200.distributed import env_rank
+    from paper_1504_01023_b200.kernels.counts import algorithmic_bytes, algorithmic_flops
+    from paper_1504_01023_b200.measure import ClockSampler, clocks_rejected, flop_peak, hbm_peak
+
+    rank, world, local = env_rank()
+    if not torch.cuda.is_available():
+        print(json.dumps({"metric": METRIC, "error": "no CUDA device"}))
+        return 1
+    torch.cuda.set_device(local)
+    distributed = launched_by_torchrun()
+    if distributed:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")           # communicator lines on stderr
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    barrier = dist.barrier if distributed else None
+    parts = [Part(*c) for c in c5_parts(world, rank)]
+    n_local = sum(p.n for p in parts)
+
+    def serial():
+        for p in parts:
+            p.L()
+
+    serial.launchers = [p.L for p in parts]
+
+    # ---- device-resident timing (the `value`) ----
+    if distributed:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local, period=0.0005)
+    step_ms = time_graph([serial], args.steps, args.warmup, sampler, barrier) / args.steps
+    part_ms = time_parts(parts, args.steps, args.warmup)
+    eager_ms = time_launches([serial], args.steps, args.warmup)[1] / args.steps
+    keys = [p.L.error_key() for p in parts]
+    if any(k != 0xFFFFFFFFFFFFFFFF for k in keys):
+        raise RuntimeError(f"C5: unexpected geometry error keys {[hex(k) for k in keys]}")
+    t = torch.tensor([step_ms, eager_ms, *part_ms], dtype=torch.float64, device="cuda")
+    if distributed:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms, eager_ms, *part_ms = t.tolist()
+    value = C5_TOTAL / (step_ms / 1e3)
+    clocks = sampler.summary()
+    sustained = ClockSampler(local, period=0.005)
+    with sustained:
+        t_end = time.time() + 1.0
+        while time.time() < t_end:
+            for _ in range(10):
+                serial()
+            torch.cuda.synchronize()
+    clocks["sustained_1s"] = sustained.summary()
+    reject = clocks_rejected(clocks) or clocks_rejected(clocks["sustained_1s"])
+
+    # ---- end to end through the public API on host batches ----
+    e2e = None
+    if not args.no_e2e:
+        e2e_steps = max(1, min(args.steps, 3))
+        ms, h2d, d2h, same = c5_e2e(parts, e2e_steps, barrier)
+        ms_pg, _, _, same_pg = c5_e2e(parts, e2e_steps, barrier, pageable=True)
+        tt = torch.tensor([ms, ms_pg], dtype=torch.float64, device="cuda")
+        if distributed:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, ms_pg = tt.tolist()
+        e2e = {"value": C5_TOTAL / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": ms, "steps": e2e_steps,
+               "api": "paper_1504_01023_b200.integrate_batch(desc, ElementBatch) -> BatchResult (numpy), "
+                      "tet batch then prism batch of this rank's shard",
+               "host_memory": "page-locked (ElementBatch.from_arrays)",
+               "bitwise_equal_to_device_path": same,
+               "pageable": {"value": C5_TOTAL / (ms_pg / 1e3), "ms_per_step": ms_pg,
+                            "host_memory": "plain numpy arrays (a reference caller's ElementBatch)",
+                            "frac_of_pinned": ms / ms_pg, "bitwise_equal_to_device_path": same_pg}}
+
+    # ---- rooflines: the dominant kernel (prism ConvDiff) and the step ----
+    hbm, hbm_src = hbm_peak()
+    fp, fp_src = flop_peak(8)
+    dom = max(range(len(parts)), key=lambda i: part_ms[i])
+    p = parts[dom]
+    tag = f"{p.desc.short_name()}_f64"
+    by = algorithmic_bytes(p.desc.element, p.desc.problem) * p.n
+    fl = algorithmic_flops(p.desc.element, p.desc.problem) * p.n
+    t_s = part_ms[dom] / 1e3
+    prof = load_profile_record(tag) or {}
+    per = prof.get("_per_element") or {}
+    roof = {"bound": "hbm", "achieved": by / t_s / 1e9, "peak": hbm, "unit": "GB/s", "frac": by / t_s / 1e9 / hbm,
+            "traffic": (per["dram_bytes"] * p.n) if per else None,
+            "kernel": f"fek::integrate_kernel<{tag}> ({p.cfg.key} shard, {p.n} elements)",
+            "launch_ms": part_ms[dom], "algorithmic_bytes_per_launch": by, "peak_source": hbm_src,
+            "model_flops_per_launch": fl, "model_flop_frac": fl / t_s / 1e12 / fp,
+            "why_hbm": "the kernel executes fewer FP64 operations than Table 4 counts (reference-frame "
+                       "contraction, DESIGN.md 4.2): executed intensity ~3.5 flop/B is below the "
+                       "FP64/HBM ridge, so HBM is its binding roof",
+            "traffic_source": f"ncu dram bytes/element of {prof.get('report')} x elements" if per else None}
+    if per.get("fp64_flops"):
+        roof["executed_fp64_tflops"] = per["fp64_flops"] * p.n / t_s / 1e12
+        roof["executed_fp64_frac"] = roof["executed_fp64_tflops"] / fp
+        roof["fp64_peak"] = fp
+    by_all = sum(algorithmic_bytes(q.desc.element, q.desc.problem) * q.n for q in parts)
+    fl_all = sum(algorithmic_flops(q.desc.element, q.desc.problem) * q.n for q in parts)
+    t_roof = max(by_all / (hbm * 1e9), fl_all / (fp * 1e12))
+    roof["step"] = {"bound": "concurrent max(sum bytes/HBM, sum model flops/FP64)", "roof_ms": t_roof * 1e3,
+                    "frac": t_roof / (step_ms / 1e3), "hbm_frac": by_all / (hbm * 1e9) / (step_ms / 1e3),
+                    "per_kernel_ms": {q.cfg.key: m for q, m in zip(parts, part_ms)}}
+
+    out = None
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic: the reference's unit-cube meshes and seeded U(-1,1) coefficients, generated "
+                       "in HBM (device PCG64 + mesh generator, bit-identical to numpy / feklab.mesh)",
+               "config": {"workload": C5_WORKLOAD, "elements_total": C5_TOTAL, "elements_per_gpu_rank0": n_local,
+                          "parts": {q.cfg.key: {"elements_this_rank": q.n, "first": q.lo,
+                                                "descriptor": q.desc.short_name()} for q in parts},
+                          "parallelism": f"element-range shards x{world} of both batches (no collective on the "
+                                         "hot path)",
+                          "l2": f"per-step traffic {by_all / 1e9:.1f} GB per GPU >> 126 MiB L2 (no reuse)"},
+               "clocks": clocks, "e2e": e2e, "gpu_launches": len(parts) * args.steps, "roofline": roof,
+               "timing": "K steps (tet + prism launch each) captured as one CUDA graph, one timed replay "
+                         "between CUDA events on its stream; max over ranks",
+               "eager": {"ms_per_step": eager_ms, "timing": "same steps on an eager stream"}}
+        if reject:
+            out["clocks_warning"] = reject
+
+    # ---- CPU baseline + parity on its sample (rank 0, N=1) ----
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle.cpu_baseline import cpu_cores
+
+        cores = cpu_cores()
+        procs = args.cpu_processes or cores["logical"] or 1
+        sample = 1 << 22
+        per_elem, err, checked = c5_cpu_baseline(parts, sample, procs)
+        t_full = sum(mesh.bench_configs()[k].spec.n_elements * v for k, v in per_elem.items())
+        out["cpu_baseline"] = {"value": C5_TOTAL / t_full, "unit": UNIT, "cores": procs, "kind": "port",
+                               "sample": f"first {sample} elements of each C5 batch, bitwise numpy port of feklab "
+                                         f"integrate_batch on {procs} processes, extrapolated to the C5 mix",
+                               "seconds_per_element": per_elem, "host_cores": cores}
+        out["parity"] = {"workload": "C5 (both batches)", "elements_checked": checked, "max_rel_frobenius": err,
+                         "tolerance": 1e-12, "pass": err <= 1e-12,
+                         "against": "numpy port, bitwise-pinned to the reference (tests/golden)"}
+
+    verify_parts = [(q.desc, q.lo, q.n, q.cfg.key, q.L) for q in parts]
+    # ---- single-configuration cases (N=1) ----
+    if rank == 0 and world == 1 and not args.no_cases:
+        verify_parts = []
+        del parts[:]
+        torch.cuda.empty_cache()
+        cases = {}
+        for key in [c for c in args.cases.split(",") if c]:
+            try:
+                cases[key] = measure_case(key, args.steps, args.warmup)
+            except Exception as exc:  # keep the headline line even if a case fails
+                cases[key] = {"error": f"{type(exc).__name__}: {exc}"}
+        out["cases"] = cases
+
+    if distributed:
+        ver = c5_verify(verify_parts)
+        if rank == 0:
+            out["verification"] = ver
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if distributed:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
 
 
 def run_ours(args) -> int:
@@ -641,8 +924,7 @@ def run_ours(args) -> int:
         cases = {}
         for key in [c for c in args.cases.split(",") if c]:
             try:
-                cases[key] = measure_c5(args.steps, args.warmup) if key == "C5" else \
-                    measure_case(key, args.steps, args.warmup)
+                cases[key] = measure_case(key, args.steps, args.warmup)
             except Exception as exc:  # keep the headline line even if a case fails
                 cases[key] = {"error": f"{type(exc).__name__}: {exc}"}
         out["cases"] = cases
@@ -663,46 +945,6 @@ def run_ours(args) -> int:
                                    "collectives": "NCCL all_reduce(MIN error key, SUM checksums) after timing"}
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if distributed:
-        dist.barrier()
-        dist.destroy_process_group()
-    return 0
-
-
-def run_c5(args) -> int:
-    """--config C5: the 64M mixed mesh, strong scaling (each rank generates and integrates its shard)."""
-    import torch
-    import torch.distributed as dist
-
-    from paper_1504_01023_b200.distributed import env_rank
-    from paper_1504_01023_b200.measure import ClockSampler, clocks_rejected
-
-    rank, world, local = env_rank()
-    torch.cuda.set_device(local)
-    distributed = launched_by_torchrun()
-    if distributed:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        dist.barrier()
-    sampler = ClockSampler(local, period=0.0005)
-    rec = measure_c5(args.steps, args.warmup, world, rank, sampler, barrier=dist.barrier if distributed else None)
-    t = torch.tensor([rec["ms_per_step"]], dtype=torch.float64, device="cuda")
-    if distributed:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    total = 64_156_250
-    if rank == 0:
-        clocks = sampler.summary()
-        line = {"metric": METRIC, "value": total / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic: reference meshes generated in HBM (device PCG64, bit-identical to numpy)",
-                "config": {"workload": rec["workload"], "elements_total": total,
-                           "parallelism": f"element-range shards x{world} of both batches, no collective"},
-                "clocks": clocks, "e2e": None, "gpu_launches": 2 * args.steps,
-                "roofline": rec["roofline"], "parity_rank0": rec["parity"]}
-        if clocks_rejected(clocks):
-            line["clocks_warning"] = clocks_rejected(clocks)
-        print(json.dumps(line), flush=True)
     if distributed:
         dist.barrier()
         dist.destroy_process_group()

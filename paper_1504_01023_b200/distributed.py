@@ -110,6 +110,13 @@ def allreduce_sums(f, u, group=None):
     """SUM-reduce the verification sums across ranks (in place); returns (f, u)."""
     import torch.distributed as dist
 
+    if dist.get_backend(group) != "nccl" and f.is_cuda:  # gloo (CPU tests, one-GPU multi-rank runs)
+        fc, uc = f.cpu(), u.cpu()
+        dist.all_reduce(fc, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(uc, op=dist.ReduceOp.SUM, group=group)
+        f.copy_(fc)
+        u.copy_(uc)
+        return f, u
     dist.all_reduce(f, op=dist.ReduceOp.SUM, group=group)
     dist.all_reduce(u, op=dist.ReduceOp.SUM, group=group)
     return f, u

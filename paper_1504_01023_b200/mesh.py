@@ -82,9 +82,10 @@ def _tet_rows(spec: MeshSpec, cells: slice | None = None) -> np.ndarray:
     return rows.reshape(-1, 12)
 
 
-def _prism_rows(spec: MeshSpec) -> np.ndarray:
+def _prism_rows(spec: MeshSpec, cells: slice | None = None) -> np.ndarray:
     hx, hy = 1.0 / spec.nx, 1.0 / spec.ny
-    ix, iy = np.divmod(np.arange(spec.nx * spec.ny), spec.ny)
+    cell = np.arange(spec.nx * spec.ny)
+    ix, iy = np.divmod(cell[cells] if cells is not None else cell, spec.ny)
     x0, y0 = ix * hx, iy * hy
     x1, y1 = x0 + hx, y0 + hy
     tris = (((x0, y0), (x1, y0), (x0, y1)), ((x1, y0), (x1, y1), (x0, y1)))
@@ -174,6 +175,27 @@ def config_rows(cfg: BenchConfig) -> tuple[np.ndarray, np.ndarray]:
     if cfg.jitter_seed is not None:
         geo = jitter_top_faces(geo, cfg.spec, cfg.jitter_seed)
     return geo, coefficient_rows(cfg.spec.n_elements, cfg.problem, cfg.spec.element_type, cfg.coeff_seed)
+
+
+def config_window(cfg: BenchConfig, n: int) -> tuple[np.ndarray, np.ndarray]:
+    """Host rows of the FIRST n elements of a configuration, without generating the rest.
+
+    Element order is cell-major (6 tets / 2 prisms per cell) and every random stream is
+    drawn row by row, so these are exactly rows [0, n) of ``config_rows(cfg)``.
+    """
+    spec = cfg.spec
+    n = min(int(n), spec.n_elements)
+    per_cell = 6 if spec.element_type is ElementType.TETRAHEDRON else 2
+    cells = slice(0, -(-n // per_cell))
+    rows_fn = _tet_rows if spec.element_type is ElementType.TETRAHEDRON else _prism_rows
+    geo = rows_fn(spec, cells)[:n]
+    if cfg.jitter_seed is not None:
+        h = np.array([1.0 / spec.nx, 1.0 / spec.ny])
+        off = np.random.default_rng(cfg.jitter_seed).uniform(-1.0, 1.0, size=(n, 3, 2)) * (0.15 * h)
+        geo = geo.reshape(-1, 6, 3).copy()
+        geo[:, 3:, :2] += off
+        geo = geo.reshape(-1, 18)
+    return geo, coefficient_rows(n, cfg.problem, spec.element_type, cfg.coeff_seed)
 
 
 # ---------------------------------------------------------------------------
