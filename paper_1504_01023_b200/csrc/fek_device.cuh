@@ -138,6 +138,14 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
                : "memory");
 }
 
+__device__ __forceinline__ uint4 pack2(double a, double b) {
+  return make_uint4(static_cast<uint32_t>(__double2loint(a)), static_cast<uint32_t>(__double2hiint(a)),
+                    static_cast<uint32_t>(__double2loint(b)), static_cast<uint32_t>(__double2hiint(b)));
+}
+__device__ __forceinline__ uint2 pack1(double a) {
+  return make_uint2(static_cast<uint32_t>(__double2loint(a)), static_cast<uint32_t>(__double2hiint(a)));
+}
+
 __device__ __forceinline__ uint2 lds64(uint32_t addr) {
   uint2 v;
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr) : "memory");

@@ -1069,6 +1069,235 @@ __device__ __forceinline__ void integrate_prism_poisson_ref(const prism_ref::Col
   });
 }
 
+// ---------------------------------------------------------------------------
+// prism ConvDiff fp64 (QSS) split over a LANE PAIR by zeta level.
+//
+// integrate_prism_cd_ref's per-level sums SXX/SXY/SYX/SbX depend only on that level's Jacobian
+// columns 0/1 (6 entries) and the shared column-2 entries J2 (9), so lane z of a pair runs the
+// three points of level z alone -- no point work is duplicated, only the 9 J2 entries and the
+// degeneracy bound.  Each lane then forms, from its own sums, its level's contribution to all 36
+// stiffness entries (and 6 load entries), sends the partner the half belonging to the partner's
+// row block (rows b = 1 - z: 18 + 3 doubles over __shfl_xor) and adds the half it receives: lane z
+// owns rows a + 3z.  Half the accumulators per thread (39 instead of 78 live sums) lets two CTAs
+// of 256 threads (16 warps/SM) run at <= 128 registers where the one-thread kernel holds 8 warps
+// at 255 registers + spill.  Both lanes execute one instruction stream: level-dependent constants
+// are selected once per thread, and J01 is formed with the reference's rounding (the level's
+// _axpy_fixed coefficients differ only in value, never in zero/+-1 pattern).
+// ---------------------------------------------------------------------------
+
+namespace prism_pair {
+using prism_ref::S;
+using prism_ref::lam;
+using prism_ref::ell;
+using prism_ref::sym_index;
+
+// sum_v c_v x_v with the reference's _axpy_fixed rounding for coefficients c_v = C(v) (all nonzero,
+// none +-1: products rounded, summed left to right); `x(v)` / `C(v)` may select at run time
+template <typename R, int NV, class Cf, class Xf>
+__device__ __forceinline__ R axpy_exact(Cf &&C, Xf &&x) {
+  R acc = C(std::integral_constant<int, 0>{}) * x(0);
+  static_for<NV - 1>([&](auto vc) {
+    constexpr int v = decltype(vc)::value + 1;
+    acc = acc + C(std::integral_constant<int, v>{}) * x(v);
+  });
+  return acc;
+}
+
+// The pair's shared geometry, split between the two lanes (both lanes end with all of it):
+//  * bound = NEAR_TOL_FACTOR * 1e-14 * diag^3 (batched.py:136-148): lane z takes the min/max of
+//    coordinate dimension z, both take dimension 2; the partner's span^2 arrives by shuffle and
+//    the sum keeps the reference's order (s0 + s1) + s2;
+//  * J2[t][i] = sum_v ld[2t][v][2] X[v][i] (coefficients -+lam_a(t)/2, never 0 or +-1): lane z
+//    forms triangle point t = z and J2[2][z], both form J2[2][2], the other four arrive by shuffle;
+//  * this level's J01[i][k] = sum_v ld[z][v][k] X[v][i]: the level coefficients +-l_b(z) differ
+//    from the other level's only in value (same zero / sign pattern), selected at run time.
+// All entries are bitwise the reference's (jac_entry<PRISM, q, k> / degeneracy_tolerance).
+template <typename R>
+__device__ __forceinline__ void level_geometry(const R (&X)[18], int z, R &bound, R (&J2)[3][3], R (&J01)[3][2]) {
+  constexpr unsigned FULL = 0xffffffffu;
+  // -- bounding box
+  auto span2 = [&](auto pick) {
+    R hi = pick(0), lo = pick(0);
+#pragma unroll
+    for (int v = 1; v < 6; ++v) {
+      hi = fmax(hi, pick(v));
+      lo = fmin(lo, pick(v));
+    }
+    const R sp = hi - lo;
+    return sp * sp;
+  };
+  const R mine = span2([&](int v) { return z ? X[3 * v + 1] : X[3 * v]; });  // dimension z
+  const R s2 = span2([&](int v) { return X[3 * v + 2]; });
+  const R theirs = __shfl_xor_sync(FULL, mine, 1);
+  const R s0 = z ? theirs : mine, s1 = z ? mine : theirs;
+  bound = R(NEAR_TOL_FACTOR) * (R(1e-14) * cube_rn(sqrt((s0 + s1) + s2)));
+  // -- zeta column at the triangle points
+  R own[3];  // J2[z][i]
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    own[i] = axpy_exact<R, 6>([&](auto vc) { FEK_CI(v, vc); return z ? R(S::ld(2, v, 2)) : R(S::ld(0, v, 2)); },
+                              [&](int v) { return X[3 * v + i]; });
+  const R j2z = axpy_exact<R, 6>([&](auto vc) { FEK_CI(v, vc); return R(S::ld(4, v, 2)); },
+                                 [&](int v) { return z ? X[3 * v + 1] : X[3 * v]; });  // J2[2][z]
+  J2[2][2] = axpy_exact<R, 6>([&](auto vc) { FEK_CI(v, vc); return R(S::ld(4, v, 2)); },
+                              [&](int v) { return X[3 * v + 2]; });
+  const R j2o = __shfl_xor_sync(FULL, j2z, 1);
+  J2[2][0] = z ? j2o : j2z;
+  J2[2][1] = z ? j2z : j2o;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const R other = __shfl_xor_sync(FULL, own[i], 1);
+    J2[0][i] = z ? other : own[i];
+    J2[1][i] = z ? own[i] : other;
+  }
+  // -- this level's columns 0/1
+  const R lo = z ? R(ell(1, 0)) : R(ell(0, 0));  // bottom-face factor l_0(z)
+  const R hi = z ? R(ell(1, 1)) : R(ell(0, 1));  // top-face factor l_1(z)
+  static_for<2>([&](auto kc) {
+    FEK_CI(k, kc);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      R acc = R(0);
+      bool any = false;
+      static_for<6>([&](auto vc) {
+        FEK_CI(v, vc);
+        constexpr double c0 = S::ld(0, v, k), c1 = S::ld(1, v, k);
+        constexpr double sgn = (k == 0 ? prism_ref::dlx : prism_ref::dly)[v % 3];
+        static_assert((c0 == 0.0) == (sgn == 0.0) && (c1 == 0.0) == (sgn == 0.0), "level zero pattern");
+        static_assert(c0 == sgn * ell(0, v / 3) && c1 == sgn * ell(1, v / 3), "level coefficients");
+        static_assert(c0 != 1.0 && c0 != -1.0 && c1 != 1.0 && c1 != -1.0, "no unit coefficients");
+        if constexpr (sgn != 0.0) {
+          const R m = (v < 3 ? lo : hi) * X[3 * v + i];  // (+-l) * x rounds like +-(l * x)
+          if (!any) {
+            acc = sgn > 0 ? m : -m;
+            any = true;
+          } else {
+            acc = sgn > 0 ? acc + m : acc - m;
+          }
+        }
+      });
+      J01[i][k] = acc;
+    }
+  });
+}
+static_assert(S::ld(2, 0, 2) != 0.0 && S::ld(0, 0, 2) != 0.0 && S::ld(4, 0, 2) != 0.0, "zeta column coefficients");
+
+template <typename R>
+__device__ __forceinline__ void integrate_cd_level(const R (&J2)[3][3], const R (&J01)[3][2], const R (&c)[20],
+                                                   R bound, int z, R (&Ah)[18], R (&Bh)[3], int &kind,
+                                                   int &kind_point) {
+  using prism_ref::mac;
+  using prism_ref::xdot;
+  constexpr double w = S::w(0);
+  // w folded into K and the load terms once per element (K' = w K, e' = w e); the zeta-derivative
+  // factor l'_b = -+1/2 folded into the accumulation constants of SXY / SYX / SYY / SbY
+  const R wc00 = R(w) * c[0];
+  const R wc0[3] = {R(w) * c[1], R(w) * c[2], R(w) * c[3]};
+  const R wcc[3] = {R(w) * c[4], R(w) * c[8], R(w) * c[12]};
+  const R wd[4] = {R(w) * c[16], R(w) * c[17], R(w) * c[18], R(w) * c[19]};
+  R SXX[3][3], SXY[3][3], SYX[3][3], SbX[3], SYY[6], SbY[3];
+  unsigned fail_mask = 0, near_mask = 0;
+  static_for<3>([&](auto tc) {
+    FEK_CI(t, tc);
+    constexpr bool F = (t == 0);
+    const R Jt[3] = {J2[t][0], J2[t][1], J2[t][2]};
+    R adj[3][3];
+    const R det = prism_ref::adjugate(J01, Jt, adj);
+    fail_mask |= prism_ref::kind_bits(det, bound, 2 * t + z, near_mask);
+    const R rdet = R(w) * recip(det);
+    R K[4][4];
+    K[0][0] = det * wc00;
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      K[0][1 + l] = fma(wc0[0], adj[l][0], fma(wc0[1], adj[l][1], wc0[2] * adj[l][2]));
+      K[1 + l][0] = fma(adj[l][0], wcc[0], fma(adj[l][1], wcc[1], adj[l][2] * wcc[2]));
+    }
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      R M[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        M[i] = fma(c[4 * (1 + i) + 1], adj[l][0], fma(c[4 * (1 + i) + 2], adj[l][1], c[4 * (1 + i) + 3] * adj[l][2]));
+#pragma unroll
+      for (int k = 0; k < 3; ++k) K[1 + k][1 + l] = rdet * fma(adj[k][0], M[0], fma(adj[k][1], M[1], adj[k][2] * M[2]));
+    }
+    const R L[3] = {R(lam(t, 0)), R(lam(t, 1)), R(lam(t, 2))};
+    static_for<3>([&](auto apc) {
+      FEK_CI(ap, apc);
+      R v[3];
+#pragma unroll
+      for (int al = 0; al < 3; ++al) v[al] = xdot<ap, true>(R(0), L[ap], K[al][0], K[al][1], K[al][2]);
+      static_for<3>([&](auto ac) {
+        FEK_CI(a, ac);
+        SXX[a][ap] = xdot<a, F>(SXX[a][ap], L[a], v[0], v[1], v[2]);
+      });
+    });
+    static_for<3>([&](auto ac) {
+      FEK_CI(a, ac);
+      const R p = xdot<a, true>(R(0), L[a], K[0][3], K[1][3], K[2][3]);
+      const R q = xdot<a, true>(R(0), L[a], K[3][0], K[3][1], K[3][2]);
+      static_for<3>([&](auto bc) {
+        FEK_CI(ap, bc);
+        mac<F>(SXY[a][ap], R(0.5 * lam(t, ap)), p);   // SXY / 2
+        mac<F>(SYX[ap][a], R(0.5 * lam(t, ap)), q);   // SYX / 2
+      });
+    });
+    static_for<3>([&](auto ac) {
+      FEK_CI(a, ac);
+      static_for<3>([&](auto bc) {
+        FEK_CI(ap, bc);
+        if constexpr (ap >= a) mac<F>(SYY[sym_index(a, ap)], R(0.25 * lam(t, a) * lam(t, ap)), K[3][3]);  // SYY / 4
+      });
+    });
+    const R e0 = det * wd[0];
+    R e[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) e[k] = fma(adj[k][0], wd[1], fma(adj[k][1], wd[2], adj[k][2] * wd[3]));
+    static_for<3>([&](auto ac) {
+      FEK_CI(a, ac);
+      SbX[a] = xdot<a, F>(SbX[a], L[a], e0, e[0], e[1]);
+      mac<F>(SbY[a], R(0.5 * lam(t, a)), e[2]);                        // SbY / 2
+    });
+  });
+  // the element's classification: both levels' points (lane z holds q = 2t + z)
+  fail_mask |= __shfl_xor_sync(0xffffffffu, fail_mask, 1);
+  near_mask |= __shfl_xor_sync(0xffffffffu, near_mask, 1);
+  first_failure(fail_mask, near_mask, kind, kind_point);
+
+  // this level's share of A_(a,b)(a',b') = sum_z [l_b l_b' SXX + l_b l'_b' SXY + l'_b l_b' SYX]
+  // + l'_b l'_b' SYY (w already in K) and of b_(a,b) = sum_z l_b SbX + l'_b SbY, for the own row
+  // block b = z (l_b(z) = ell(z, z)) and the partner's b = 1 - z (ell(z, 1 - z)); with the
+  // halves folded in, l'_b' terms are +-1 (compile-time signs) and l'_b = s (s = -1, +1 for b = 0, 1)
+  static_assert(ell(0, 0) == ell(1, 1) && ell(0, 1) == ell(1, 0), "level factors swap between the levels");
+  const R sgn = z ? R(1) : R(-1);                                          // l'_own / (1/2)
+  const R lcol[2] = {z ? R(ell(1, 0)) : R(ell(0, 0)), z ? R(ell(1, 1)) : R(ell(0, 1))};  // l_b'(z)
+  constexpr double l_own = ell(0, 0), l_oth = ell(0, 1);
+  R Po[18], Bo[3];  // the partner's row block: sent
+  static_for<3>([&](auto ac) {
+    FEK_CI(a, ac);
+    static_for<3>([&](auto bc) {
+      FEK_CI(ap, bc);
+      const R syy = SYY[sym_index(a, ap)];
+      static_for<2>([&](auto b2c) {
+        FEK_CI(bp, b2c);
+        const R u = bp ? fma(lcol[bp], SXX[a][ap], SXY[a][ap]) : fma(lcol[bp], SXX[a][ap], -SXY[a][ap]);
+        const R v = bp ? fma(lcol[bp], SYX[a][ap], syy) : fma(lcol[bp], SYX[a][ap], -syy);
+        const R sv = sgn * v;
+        Ah[6 * a + ap + 3 * bp] = fma(R(l_own), u, sv);
+        Po[6 * a + ap + 3 * bp] = fma(R(l_oth), u, -sv);
+      });
+    });
+    const R sb = sgn * SbY[a];
+    Bh[a] = fma(R(l_own), SbX[a], sb);
+    Bo[a] = fma(R(l_oth), SbX[a], -sb);
+  });
+#pragma unroll
+  for (int j = 0; j < 18; ++j) Ah[j] = Ah[j] + __shfl_xor_sync(0xffffffffu, Po[j], 1);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) Bh[j] = Bh[j] + __shfl_xor_sync(0xffffffffu, Bo[j], 1);
+}
+}  // namespace prism_pair
+
 // QSS prism kernels from the element's distinct Jacobian columns (computed by
 // the caller, so the input stage can be released before the math starts)
 template <typename R, int PB, class Coef>

@@ -57,8 +57,19 @@ struct Traits {
   static constexpr int DSG = 3 * NV;
   static constexpr int DSC = (PB == POISSON) ? NQ : 20;
   static constexpr int NA = NS * NS;
-  static constexpr int THREADS = 128;
-  static constexpr int TILE = THREADS;
+  // fp64 prism ConvDiff (QSS, reference frame): each element on a lane pair, one zeta level per
+  // lane (fek_element.cuh prism_pair; FEK_PRISM_PAIR=0 builds the one-thread kernel instead)
+#ifndef FEK_PRISM_PAIR
+#define FEK_PRISM_PAIR 1
+#endif
+#ifndef FEK_PAIR_TILE
+#define FEK_PAIR_TILE 64
+#endif
+  static constexpr bool PAIR = FEK_PRISM_PAIR && ET == PRISM && PB == CONV_DIFF && GEO == GEO_GENERIC &&
+                               VAR == QSS && sizeof(R) == 8;
+  static constexpr int TILE = PAIR ? FEK_PAIR_TILE : 128;  // elements per tile (a multiple of every lane width)
+  static constexpr int LANES = PAIR ? 2 : 1;
+  static constexpr int THREADS = TILE * LANES;
   // prisms (and the re-computing generic variants) re-read coordinates from
   // the staged tile instead of pinning 18 reals in registers
   static constexpr bool LAZY_X = (GEO == GEO_GENERIC) && (ET == PRISM || VAR != QSS);
@@ -84,8 +95,9 @@ struct Traits {
   static constexpr int STAGES_ = F32_PRISM_CD ? 2 :
       ((PRISM_P || (LAZY_X && PB == CONV_DIFF)) ? 1 : ((ET == TET && PB == POISSON) ? 3 : 2));
   static constexpr int MIN_BLOCKS_ = (F32_PRISM_CD || PRISM_P || (ET == TET && PB == POISSON)) ? 3 : 2;
+  // (PAIR: 2 CTAs x 256 threads = 16 warps/SM at <= 128 registers)
   static constexpr int STAGES = P32 ? 2 : STAGES_;
-  static constexpr int MIN_BLOCKS = P32 ? 4 : MIN_BLOCKS_;
+  static constexpr int MIN_BLOCKS = P32 ? 4 : (PAIR ? 256 / TILE : MIN_BLOCKS_);
   static constexpr unsigned GEO_TILE_BYTES = TILE * DSG * sizeof(R);
   static constexpr unsigned COEF_TILE_BYTES = TILE * DSC * sizeof(R);
   static constexpr unsigned OUT_A_BYTES = TILE * NA * sizeof(R);
@@ -214,6 +226,80 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
     };
     const long long e0 = t * K::TILE;
     const int count = static_cast<int>(min(static_cast<long long>(K::TILE), p.n - e0));
+    if constexpr (K::PAIR) {
+      // element el on lanes (2 el, 2 el + 1), lane z = zeta level (fek_element.cuh prism_pair).
+      // Every thread runs the math, also past `count` (on stale stage data, results dropped), so
+      // both lanes of a pair always meet at the shuffles.
+      const int el = tid >> 1, z = tid & 1;
+      const bool act = !stop && el < count;
+      R Ah[18], Bh[3];
+      int kind = 0, kind_point = -1;
+      {
+        R C[20], J2[3][3], J01[3][2], bound;
+        RowIO<R, 20>::load(pipe.coef(s), el, p.lane_width, C);
+        {
+          R X[18];
+          RowIO<R, 18>::load(pipe.geo(s), el, p.lane_width, X);
+          prism_pair::level_geometry(X, z, bound, J2, J01);
+        }
+        if (!release()) break;
+        prism_pair::integrate_cd_level(J2, J01, C, bound, z, Ah, Bh, kind, kind_point);
+      }
+      if (act && z == 0 && kind) atomicMin(p.error_key, make_error_key(p.base + e0 + el, kind_point, kind));
+      if (tid == 0) bulk_wait_read<0>();
+      __syncthreads();
+      constexpr unsigned RB = sizeof(R);
+      if (p.out_packed) {
+        constexpr int DSO = 42;
+        const int w = p.out_width;
+        const int padded = ((count + w - 1) / w) * w;
+        if (el < padded) {
+          const R nan = R(__longlong_as_double(0x7ff8000000000000ll));
+          if (w == 1) {
+            const uint32_t row = out_a + static_cast<uint32_t>(el) * DSO * RB;
+#pragma unroll
+            for (int c = 0; c < 9; ++c)
+              sts128(row + 144u * z + 16u * c, pack2(act ? Ah[2 * c] : nan, act ? Ah[2 * c + 1] : nan));
+#pragma unroll
+            for (int j = 0; j < 3; ++j) sts64(row + 288u + 24u * z + 8u * j, pack1(act ? Bh[j] : nan));
+          } else {
+            const uint32_t base = out_a + static_cast<uint32_t>((el / w) * w * DSO + (el % w)) * RB;
+            const uint32_t stride = static_cast<uint32_t>(w) * RB;
+#pragma unroll
+            for (int j = 0; j < 18; ++j) sts64(base + (18u * z + j) * stride, pack1(act ? Ah[j] : nan));
+#pragma unroll
+            for (int j = 0; j < 3; ++j) sts64(base + (36u + 3u * z + j) * stride, pack1(act ? Bh[j] : nan));
+          }
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+          const unsigned ob = padded * DSO * RB;
+          char *go = static_cast<char *>(p.stiffness) + e0 * DSO * RB;
+          bulk_store(go, out_a, ob);  // 336-byte rows: always a multiple of 16
+          bulk_commit();
+        }
+        continue;
+      }
+      if (act) {
+        // rows a + 3z of the element's 6x6 block (144 contiguous bytes): lanes 0..7 of a phase hit
+        // 16-byte bank groups (18 el + 9 z + c) mod 8, all distinct
+        const uint32_t row = out_a + static_cast<uint32_t>(el) * 36u * RB + 144u * z;
+#pragma unroll
+        for (int c = 0; c < 9; ++c) sts128(row + 16u * c, pack2(Ah[2 * c], Ah[2 * c + 1]));
+#pragma unroll
+        for (int j = 0; j < 3; ++j) sts64(out_b + static_cast<uint32_t>(el) * 6u * RB + 24u * z + 8u * j, pack1(Bh[j]));
+      }
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (tid == 0) {
+        const unsigned ab = count * K::NA * RB, bb = count * K::NS * RB;  // fp64 rows: multiples of 16
+        bulk_store(static_cast<char *>(p.stiffness) + e0 * K::NA * RB, out_a, ab);
+        bulk_store(static_cast<char *>(p.load) + e0 * K::NS * RB, out_b, bb);
+        bulk_commit();
+      }
+      continue;
+    }
     const bool active = !stop && tid < count;
     const long long e_abs = p.base + e0 + tid;
     R C[K::DSC];
