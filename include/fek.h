@@ -14,6 +14,8 @@
  *                          whole, on HOST arrays (ElementBatch.geometry_data /
  *                          coefficient_data in, BatchResult.stiffness / load
  *                          out): chunked H2D -> kernel -> D2H pipeline.
+ *   fek_integrate_host_staged <- the same for pageable host arrays (staged
+ *                          through page-locked buffers by host copy threads).
  *   fek_classify        <- batched.py:136-177  _bbox_scale + _adjugate +
  *                          _check_dets with the reference's rounding: the exact
  *                          first-error key when fek_integrate reports NEAR.
@@ -158,6 +160,18 @@ int fek_integrate_host(const fek_batch_desc *d, void *device_workspace, size_t w
  * Call it when fek_integrate's key decodes to FEK_KIND_NEAR; the result is then
  * FEK_NO_ERROR (the batch is valid) or a DEGENERATE / INVERTED key. */
 int fek_classify(const fek_batch_desc *d, void *cuda_stream);
+
+/* fek_integrate_host for PAGEABLE host buffers (plain malloc / numpy memory, as a reference
+ * caller's ElementBatch holds them, layout.py:103-112): every pageable array among geometry /
+ * coefficients / stiffness / load is staged through `host_staging` (page-locked, at least
+ * fek_host_staging_bytes(d, n_streams, chunk_elements) bytes, 16-byte aligned) by
+ * `copy_threads` host threads, chunk by chunk, so the host copies of chunk i overlap the DMA
+ * and the kernels of chunks i-1, i-2; page-locked arrays are DMA'd directly.  Otherwise as
+ * fek_integrate_host (same error semantics). */
+size_t fek_host_staging_bytes(const fek_batch_desc *d, int n_streams, int64_t chunk_elements);
+int fek_integrate_host_staged(const fek_batch_desc *d, void *device_workspace, size_t workspace_bytes, int n_streams,
+                              void *const *cuda_streams, int64_t chunk_elements, void *host_staging,
+                              size_t staging_bytes, int copy_threads, unsigned long long *error_key_out);
 
 /* Split an error key.  point = -1 on the element-constant (geo_linear) path. */
 int fek_decode_error(unsigned long long key, int64_t *element, int32_t *point, int32_t *kind);

@@ -72,6 +72,10 @@ SIGNATURES = {
     "fek_host_workspace_bytes": (ctypes.c_size_t, [_DP, ctypes.c_int, ctypes.c_int64]),
     "fek_integrate_host": (ctypes.c_int, [_DP, _P, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(_P),
                                           ctypes.c_int64, ctypes.POINTER(ctypes.c_ulonglong)]),
+    "fek_host_staging_bytes": (ctypes.c_size_t, [_DP, ctypes.c_int, ctypes.c_int64]),
+    "fek_integrate_host_staged": (ctypes.c_int, [_DP, _P, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(_P),
+                                                 ctypes.c_int64, _P, ctypes.c_size_t, ctypes.c_int,
+                                                 ctypes.POINTER(ctypes.c_ulonglong)]),
     "fek_decode_error": (ctypes.c_int, [ctypes.c_ulonglong, ctypes.POINTER(ctypes.c_int64),
                                         ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
     "fek_classify": (ctypes.c_int, [_DP, _P]),

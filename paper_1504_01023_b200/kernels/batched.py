@@ -558,6 +558,31 @@ def host_chunk_elements(n: int) -> int:
     return -(-chunk // 128) * 128
 
 
+_staging: dict[int, np.ndarray] = {}
+
+
+def _needs_staging(*arrays) -> bool:
+    """A large pageable input: DMA from it would serialise in the driver's own bounce buffers."""
+    return any(a.nbytes >= hostmem.PIN_THRESHOLD_BYTES and not hostmem.is_pinned(a) for a in arrays)
+
+
+def _staging_buffer(device: int, nbytes: int) -> np.ndarray:
+    """Page-locked staging for fek_integrate_host_staged, kept per device and grown on demand."""
+    with _stream_lock:
+        buf = _staging.get(device)
+        if buf is None or buf.nbytes < nbytes:
+            buf = _staging[device] = hostmem.empty(-(-nbytes // 8), pin=True)
+        return buf
+
+
+def _copy_threads() -> int:
+    """Host copy threads of the staged pipeline: this rank's share of the host cores (<= 16)."""
+    import os
+
+    per_node = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+    return max(1, min(16, (os.cpu_count() or 1) // per_node))
+
+
 def _aligned_f64(a) -> np.ndarray:
     a = np.ascontiguousarray(a, dtype=np.float64)
     if a.ctypes.data % 16:
@@ -601,8 +626,17 @@ def _integrate_host(desc: KernelDescriptor, batch, out_layout, base_index: int, 
         s.wait_stream(cur)
     handles = (ctypes.c_void_p * len(streams))(*[s.cuda_stream for s in streams])
     key = ctypes.c_ulonglong(_native.NO_ERROR)
-    status = lib.fek_integrate_host(ctypes.byref(dd), ws.data_ptr(), ws_bytes, len(streams), handles, chunk,
-                                    ctypes.byref(key))
+    if _needs_staging(geo, cof):
+        # a caller's pageable arrays (e.g. a feklab ElementBatch): staged through page-locked
+        # buffers by host copy threads, overlapped with the DMA and the kernels
+        st_bytes = lib.fek_host_staging_bytes(ctypes.byref(dd), len(streams), chunk)
+        staging = _staging_buffer(device, st_bytes)
+        status = lib.fek_integrate_host_staged(ctypes.byref(dd), ws.data_ptr(), ws_bytes, len(streams), handles,
+                                               chunk, staging.ctypes.data, st_bytes, _copy_threads(),
+                                               ctypes.byref(key))
+    else:
+        status = lib.fek_integrate_host(ctypes.byref(dd), ws.data_ptr(), ws_bytes, len(streams), handles, chunk,
+                                        ctypes.byref(key))
     for s in streams:
         cur.wait_stream(s)
     if status == _native.ERR_GEOMETRY:

@@ -301,3 +301,62 @@ def test_flat_output_layouts():
     dres = integrate_batch(case_descriptors(TET, POISSON)[0], DeviceBatch.from_host(batch),
                            out_layout=BatchLayout(LayoutKind.LANE_INTERLEAVED, 8))
     assert np.array_equal(dres.flat_output(pad_value=0.0).cpu().numpy(), flat)
+
+
+@pytest.mark.parametrize("et,pb", [(TET, CONVDIFF), (PRISM, CONVDIFF), (PRISM, POISSON)],
+                         ids=lambda c: getattr(c, "value", c))
+def test_pageable_host_batches_are_staged_bitwise(et, pb):
+    """A caller's plain numpy (pageable) ElementBatch goes through fek_integrate_host_staged; the
+    results equal the page-locked path's bit for bit, also for a lane-interleaved layout."""
+    from paper_1504_01023_b200 import hostmem, mesh
+    from paper_1504_01023_b200.kernels import batched as KB
+    from paper_1504_01023_b200.layout import convert
+
+    spec = mesh.spec_for_element_count(et, 700_000)
+    geo = mesh.geometry_rows(spec)
+    cof = mesh.coefficient_rows(spec.n_elements, pb, et, 3)
+    pinned = ElementBatch.from_arrays(et, pb, geo, cof)
+    assert hostmem.is_pinned(pinned.geometry_data)
+    for batch in (pinned, convert(pinned, BatchLayout(LayoutKind.LANE_INTERLEAVED, 16))):
+        plain = ElementBatch(batch.element_type, batch.problem, batch.n_elements, batch.layout,
+                             np.array(batch.geometry_data), np.array(batch.coefficient_data))
+        assert not hostmem.is_pinned(plain.geometry_data) and KB._needs_staging(plain.geometry_data)
+        desc = KernelDescriptor(Variant.QSS, fek.natural_path(et), pb, et)
+        want, got = integrate_batch(desc, batch), integrate_batch(desc, plain)
+        assert np.array_equal(want.stiffness, got.stiffness) and np.array_equal(want.load, got.load)
+
+
+def test_staged_abi_with_pageable_outputs():
+    """fek_integrate_host_staged also stages PAGEABLE outputs (a C caller's malloc'd A / b)."""
+    import ctypes
+
+    import torch
+
+    from paper_1504_01023_b200 import _native, hostmem, mesh
+    from paper_1504_01023_b200.kernels.batched import _desc_struct, _host_streams
+    from paper_1504_01023_b200.layout import ELEMENT_MAJOR
+
+    et, pb = PRISM, CONVDIFF
+    spec = mesh.spec_for_element_count(et, 300_000)
+    geo = np.ascontiguousarray(mesh.geometry_rows(spec).reshape(-1))
+    cof = np.ascontiguousarray(mesh.coefficient_rows(spec.n_elements, pb, et, 4).reshape(-1))
+    n = spec.n_elements
+    A, b = np.empty((n, 6, 6)), np.empty((n, 6))
+    assert not hostmem.is_pinned(A)
+    lib = _native.load()
+    desc = KernelDescriptor(Variant.QSS, GeometryPath.GEO_GENERIC, pb, et)
+    dd = _desc_struct(desc, ELEMENT_MAJOR, n, 0, 0, geo.ctypes.data, cof.ctypes.data, A.ctypes.data, b.ctypes.data, 0)
+    streams = _host_streams(torch.cuda.current_device())
+    handles = (ctypes.c_void_p * len(streams))(*[s.cuda_stream for s in streams])
+    chunk = 65536
+    ws_bytes = lib.fek_host_workspace_bytes(ctypes.byref(dd), len(streams), chunk)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    st_bytes = lib.fek_host_staging_bytes(ctypes.byref(dd), len(streams), chunk)
+    staging = hostmem.empty(-(-st_bytes // 8), pin=True)
+    torch.cuda.synchronize()
+    key = ctypes.c_ulonglong()
+    rc = lib.fek_integrate_host_staged(ctypes.byref(dd), ws.data_ptr(), ws_bytes, len(streams), handles, chunk,
+                                       staging.ctypes.data, st_bytes, 4, ctypes.byref(key))
+    assert rc == 0 and key.value == _native.NO_ERROR
+    ref = integrate_batch(desc, ElementBatch.from_arrays(et, pb, geo.reshape(n, -1), cof.reshape(n, -1)))
+    assert np.array_equal(A, ref.stiffness) and np.array_equal(b, ref.load)
