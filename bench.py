@@ -416,7 +416,7 @@ def measure_case(key, steps, warmup, variant="qss"):
                   "timing": "eager stream, CUDA events around each launch"},
         "buffer_sets": sets, "clocks": sampler.summary(),
         "roofline": dict(case_roofline(et, pb, n, ms / 1e3, rb),
-                         traffic=load_profile_traffic(f"{desc.short_name()}_{'f32' if fp32 else 'f64'}")),
+                         traffic=load_profile_traffic(f"{desc.short_name()}_{'f32' if fp32 else 'f64'}", n)),
         "parity": {"max_rel_frobenius": err, "elements_checked": cnt, "tolerance": tol, "pass": err <= tol,
                    "against": "numpy oracle (bitwise-pinned restatement of the reference)"},
     }
@@ -440,37 +440,32 @@ def c5_parts(world: int, rank: int):
     return parts
 
 
-def load_profile_traffic(kernel_tag: str, n: int | None = None):
-    """DRAM bytes per launch of a kernel from the committed ncu summary (profiles/ncu_summary.json).
-
-    With ``n``: scaled from the captured launch's element count to n elements (the capture's
-    configuration is named in its report file, e.g. prof_C4_r01 -> C4).
-    """
+def load_profile_traffic(kernel_tag: str, n: int):
+    """DRAM bytes of one launch over n elements: the committed ncu capture's bytes per element x n."""
     rec = load_profile_record(kernel_tag)
-    if not rec or rec.get("dram_bytes_per_launch") is None:
-        return None
-    if n is None:
-        return rec["dram_bytes_per_launch"]
-    per = rec.get("_per_element")
-    return None if per is None else per["dram_bytes"] * n
+    return None if not rec else rec["_per_element"]["dram_bytes"] * n
 
 
 def load_profile_record(kernel_tag: str):
-    import re
+    """The committed ncu capture (profiles/ncu_summary.json) of a kernel, with per-element figures.
 
+    Records are keyed by the captured configuration; the C5 capture of a kernel (the headline's
+    own launch) is preferred over a single-configuration one.
+    """
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
-            rec = dict(json.load(fh).get(kernel_tag) or {})
+            data = json.load(fh)
     except Exception:
         return None
-    m = re.match(r"prof_(C\d[A-Z]?)", rec.get("report", ""))
-    if m and rec:
-        from paper_1504_01023_b200 import mesh
-
-        n = rec.get("elements") or mesh.bench_configs()[m.group(1)].spec.n_elements
-        rec["_per_element"] = {"dram_bytes": rec.get("dram_bytes_per_launch", 0) / n,
-                               "fp64_flops": rec.get("executed_fp64_flops", 0) / n, "elements_captured": n}
+    recs = [(k, dict(v)) for k, v in data.items() if v.get("kernel_tag") == kernel_tag and v.get("elements")]
+    if not recs:
+        return None
+    key, rec = sorted(recs, key=lambda kv: (not kv[0].startswith("C5"), kv[0]))[0]
+    n = rec["elements"]
+    rec["_per_element"] = {"dram_bytes": rec.get("dram_bytes_per_launch", 0) / n,
+                           "fp64_flops": rec.get("executed_fp64_flops", 0) / n, "elements_captured": n,
+                           "capture": key}
     return rec
 
 
@@ -703,7 +698,8 @@ def run_c5(args) -> int:
             "why_hbm": "the kernel executes fewer FP64 operations than Table 4 counts (reference-frame "
                        "contraction, DESIGN.md 4.2): executed intensity ~3.5 flop/B is below the "
                        "FP64/HBM ridge, so HBM is its binding roof",
-            "traffic_source": f"ncu dram bytes/element of {prof.get('report')} x elements" if per else None}
+            "traffic_source": f"ncu dram bytes/element of {prof.get('report')} x elements" if per else None,
+            "ncu_capture": prof.get("report")}
     if per.get("fp64_flops"):
         roof["executed_fp64_tflops"] = per["fp64_flops"] * p.n / t_s / 1e12
         roof["executed_fp64_frac"] = roof["executed_fp64_tflops"] / fp
@@ -875,7 +871,7 @@ def run_ours(args) -> int:
         roof = case_roofline(et, pb, n, launch_ms / 1e3)
         kernel_tag = f"{desc.short_name()}_f64"
         roof_line = {"bound": roof["bound"], "achieved": roof["achieved"], "peak": roof["peak"],
-                     "unit": roof["unit"], "frac": roof["frac"], "traffic": load_profile_traffic(kernel_tag),
+                     "unit": roof["unit"], "frac": roof["frac"], "traffic": load_profile_traffic(kernel_tag, n),
                      "algorithmic_bytes_per_launch": roof["bytes_per_launch"],
                      "peak_source": roof["peak_source"], "kernel": f"fek::integrate_kernel<{kernel_tag}>",
                      "launch_ms": launch_ms, **cfgd}

@@ -4,8 +4,9 @@
     python tools/ncu_summary.py TAG=gpurun_out/prof_C2.ncu-rep ... [--md profiles/ncu_r01.md]
 
 Run here (no GPU): reads the .ncu-rep files with `ncu -i --page raw --csv`.
-The JSON is keyed by kernel tag (descriptor_dtype), which bench.py uses to
-fill roofline.traffic (dram bytes per launch).
+The JSON is keyed by capture (benchmark configuration, e.g. C5P, C4f32); each record names its
+kernel tag (descriptor_dtype) and element count, from which bench.py scales roofline.traffic
+(DRAM bytes per element x the launch's elements).
 """
 import argparse
 import csv
@@ -104,14 +105,29 @@ def main():
     data = {}
     if os.path.exists(args.out):
         data = json.load(open(args.out))
+    import re
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_1504_01023_b200 import mesh
+
     for item in args.reports:
         tag, rep = item.split("=", 1)
-        data[tag] = read(rep)
-        data[tag]["report"] = os.path.basename(rep)
+        rec = read(rep)
+        rec["report"] = os.path.basename(rep)
+        # configuration of the capture (tools/profile_case.py --case KEY [--dtype f32]) and its kernel tag
+        cfg_key = re.sub(r"f32$", "", tag)
+        cfg = mesh.bench_configs().get(cfg_key)
+        if cfg is not None:
+            et, pb = cfg.spec.element_type.value, cfg.problem.value
+            path = "linear" if et == "tet" else "generic"
+            rec["elements"] = cfg.spec.n_elements
+            rec["kernel_tag"] = f"qss_{path}_{et}_{pb}_{'f32' if tag.endswith('f32') else 'f64'}"
+        data[tag] = rec
     with open(args.out, "w") as fh:
         json.dump(data, fh, indent=1)
     if args.md:
-        lines = ["| kernel tag | us | DRAM R+W (MB) | DRAM % peak | FP64 pipe % | FMA pipe % | executed TFLOP/s "
+        lines = ["| capture | us | DRAM R+W (MB) | DRAM % peak | FP64 pipe % | FMA pipe % | executed TFLOP/s "
                  "(FMA = 2) | warps active % | regs | top stalls |",
                  "|---|---|---|---|---|---|---|---|---|---|"]
         for tag, r in data.items():
