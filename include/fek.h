@@ -118,6 +118,11 @@ typedef struct fek_batch_desc {
                              concurrently running launch).  NULL = static
                              round-robin tiles.  fek_integrate_host ignores it
                              and keeps one queue per stream in its workspace. */
+  int32_t tile_elements;  /* elements per CTA tile (the tuner's T): 0 = the kernel's own
+                             choice; 64 / 128 / 256 for the QSS natural-path kernels
+                             (geo_linear tets, geo_generic prisms), else FEK_ERR_ARGUMENT.
+                             Results are bitwise independent of it. */
+  int32_t reserved;       /* 0 */
 } fek_batch_desc;
 
 int fek_abi_version(void);

@@ -55,6 +55,8 @@ class BatchDesc(ctypes.Structure):
         ("out_lane_width", ctypes.c_int32),
         ("ctas_per_sm", ctypes.c_int32),
         ("scheduler", ctypes.c_void_p),
+        ("tile_elements", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 

@@ -106,6 +106,12 @@ int validate(const fek_batch_desc *d, bool need_pointers) {
     return FEK_ERR_ARGUMENT;
   }
   if (d->n_elements < 0 || d->base_index < 0 || d->ctas_per_sm < 0) return FEK_ERR_ARGUMENT;
+  if (d->tile_elements != 0) {
+    const int t = d->tile_elements;
+    const bool natural = d->variant == FEK_QSS &&
+                         d->geometry_path == (d->element == FEK_TETRAHEDRON ? FEK_GEO_LINEAR : FEK_GEO_GENERIC);
+    if (!natural || !(t == 64 || t == 128 || t == 256)) return FEK_ERR_ARGUMENT;
+  }
   const bool packed = d->out_format == FEK_OUT_PACKED;
   if (!packed && d->out_format != FEK_OUT_SPLIT) return FEK_ERR_ARGUMENT;
   if (packed) {
@@ -124,7 +130,10 @@ int validate(const fek_batch_desc *d, bool need_pointers) {
 
 int launch(const fek_batch_desc *d, cudaStream_t stream, int *grid_out, int *block_out, int *smem_out,
            int *tile_out, bool do_launch) {
-  const int idx = kernel_index(d->dtype, d->element, d->problem, d->variant, d->geometry_path);
+  const int idx = d->tile_elements
+                      ? fek::tiled_index(d->dtype, d->element, d->problem,
+                                         d->tile_elements == 64 ? 0 : (d->tile_elements == 128 ? 1 : 2))
+                      : kernel_index(d->dtype, d->element, d->problem, d->variant, d->geometry_path);
   const KernelEntry &ke = kernel_table()[idx];
   if (!ke.fn) return FEK_ERR_ARGUMENT;
   LaunchGeometry lg;
@@ -427,9 +436,13 @@ SlotPlan slot_plan(const fek_batch_desc *d, long long chunk) {
 long long flat_len(long long n, int ds, int w) { return n == 0 ? 0 : ((n + w - 1) / w) * w * ds; }
 }  // namespace
 
+// host pipeline chunks: multiples of 256 elements (every tile size, hence every lane width)
+static constexpr long long kChunkAlign = 256;
+static long long round_chunk(long long c) { return ((c + kChunkAlign - 1) / kChunkAlign) * kChunkAlign; }
+
 size_t fek_host_workspace_bytes(const fek_batch_desc *d, int n_streams, int64_t chunk_elements) {
   if (!d || n_streams < 1 || chunk_elements < 1) return 0;
-  return host_header_bytes(n_streams) + static_cast<size_t>(n_streams) * slot_plan(d, chunk_elements).slot;
+  return host_header_bytes(n_streams) + static_cast<size_t>(n_streams) * slot_plan(d, round_chunk(chunk_elements)).slot;
 }
 
 }  // extern "C"
@@ -537,8 +550,8 @@ int host_pipeline(const fek_batch_desc *d, void *device_workspace, size_t worksp
   if (n_streams < 1 || !cuda_streams || chunk_elements < 1 || !error_key_out) return FEK_ERR_ARGUMENT;
   const int w = d->layout == FEK_ELEMENT_MAJOR ? 1 : d->lane_width;
   // chunk boundaries on whole lane blocks and even element counts (fp32 rows)
-  const long long align = 128;  // TILE: multiple of every lane width
-  long long chunk = ((chunk_elements + align - 1) / align) * align;
+  const long long align = kChunkAlign;
+  long long chunk = round_chunk(chunk_elements);
   if (fek_host_workspace_bytes(d, n_streams, chunk) > workspace_bytes || !device_workspace)
     return FEK_ERR_WORKSPACE;
   if (!aligned16(device_workspace)) return FEK_ERR_ALIGNMENT;
@@ -619,7 +632,7 @@ int host_pipeline(const fek_batch_desc *d, void *device_workspace, size_t worksp
     cudaStream_t st = static_cast<cudaStream_t>(cuda_streams[slot]);
     char *base = ws + header + slot * sp.slot;
     char *dg = base, *dc = base + sp.geo, *dA = dc + sp.coef, *db = dA + sp.A;
-    // lo is a multiple of 128 (hence of W): the chunk's flat range starts at lo*DS
+    // lo is a multiple of 256 (hence of W): the chunk's flat range starts at lo*DS
     const size_t gbytes = flat_len(cnt, dsg, w) * rb, cbytes = flat_len(cnt, dsc, w) * rb;
     const char *srcg = hg + lo * dsg * rb, *srcc = hc + lo * dsc * rb;
     if (pool && ci >= n_streams) {
@@ -718,7 +731,7 @@ int fek_integrate_host(const fek_batch_desc *d, void *device_workspace, size_t w
 
 size_t fek_host_staging_bytes(const fek_batch_desc *d, int n_streams, int64_t chunk_elements) {
   if (!d || n_streams < 1 || chunk_elements < 1) return 0;
-  const long long chunk = ((chunk_elements + 127) / 128) * 128;
+  const long long chunk = round_chunk(chunk_elements);
   return static_cast<size_t>(n_streams) * stage_plan(d, chunk).slot;
 }
 

@@ -17,10 +17,17 @@ struct KernelEntry {
   int tile = 0;
 };
 
-// index: dtype(2) x element(2) x problem(2) x variant(3) x path(2)
-constexpr int kIndexCount = 2 * 2 * 2 * 3 * 2;
+// index: dtype(2) x element(2) x problem(2) x variant(3) x path(2), then the tile-size variants of
+// the QSS natural-path kernels (geo_linear tets, geo_generic prisms): dtype x element x problem x
+// tile {64, 128, 256} (fek_batch_desc.tile_elements; the tuner's T dimension)
+constexpr int kBaseCount = 2 * 2 * 2 * 3 * 2;
+constexpr int kTiles[3] = {64, 128, 256};
+constexpr int kIndexCount = kBaseCount + 2 * 2 * 2 * 3;
 inline int kernel_index(int dtype, int et, int pb, int var, int geo) {
   return (((dtype * 2 + et) * 2 + pb) * 3 + var) * 2 + geo;
+}
+inline int tiled_index(int dtype, int et, int pb, int tile_slot) {
+  return kBaseCount + ((dtype * 2 + et) * 2 + pb) * 3 + tile_slot;
 }
 
 void register_f64_tet_poisson(KernelEntry *table);
@@ -56,6 +63,12 @@ void fill_case(KernelEntry *table, int dtype) {
     const KernelEntry lin = entry<Traits<R, ET, PB, QSS, GEO_LINEAR>>();
     for (int v = 0; v < 3; ++v) table[kernel_index(dtype, ET, PB, v, GEO_LINEAR)] = lin;
   }
+#ifndef FEK_NO_TILES  // (experiment builds skip the tuner's tile variants)
+  constexpr int NAT = ET == TET ? GEO_LINEAR : GEO_GENERIC;
+  table[tiled_index(dtype, ET, PB, 0)] = entry<Traits<R, ET, PB, QSS, NAT, kTiles[0]>>();
+  table[tiled_index(dtype, ET, PB, 1)] = entry<Traits<R, ET, PB, QSS, NAT, kTiles[1]>>();
+  table[tiled_index(dtype, ET, PB, 2)] = entry<Traits<R, ET, PB, QSS, NAT, kTiles[2]>>();
+#endif
 }
 #endif
 

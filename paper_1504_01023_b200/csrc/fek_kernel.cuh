@@ -48,7 +48,8 @@ struct LaunchParams {
   unsigned long long *scheduler;  // [next tile, CTAs done] or null (static round-robin)
 };
 
-template <typename R_, int ET_, int PB_, int VAR_, int GEO_>
+// TILE_ = 0: the kernel's own tile; 64 / 128 / 256: the tuner's tile-size variants (fek_dispatch.cuh)
+template <typename R_, int ET_, int PB_, int VAR_, int GEO_, int TILE_ = 0>
 struct Traits {
   using R = R_;
   static constexpr int ET = ET_, PB = PB_, VAR = VAR_, GEO = GEO_;
@@ -67,7 +68,9 @@ struct Traits {
 #endif
   static constexpr bool PAIR = FEK_PRISM_PAIR && ET == PRISM && PB == CONV_DIFF && GEO == GEO_GENERIC &&
                                VAR == QSS && sizeof(R) == 8;
-  static constexpr int TILE = PAIR ? FEK_PAIR_TILE : 128;  // elements per tile (a multiple of every lane width)
+  static constexpr int NATURAL_TILE = PAIR ? FEK_PAIR_TILE : 128;
+  static constexpr int TILE = TILE_ ? TILE_ : NATURAL_TILE;  // elements per tile (a multiple of every lane width)
+  static_assert(TILE % 64 == 0, "a tile must be a whole number of lane blocks for every lane width");
   static constexpr int LANES = PAIR ? 2 : 1;
   static constexpr int THREADS = TILE * LANES;
   // prisms (and the re-computing generic variants) re-read coordinates from
@@ -97,7 +100,9 @@ struct Traits {
   static constexpr int MIN_BLOCKS_ = (F32_PRISM_CD || PRISM_P || (ET == TET && PB == POISSON)) ? 3 : 2;
   // (PAIR: 2 CTAs x 256 threads = 16 warps/SM at <= 128 registers)
   static constexpr int STAGES = P32 ? 2 : STAGES_;
-  static constexpr int MIN_BLOCKS = P32 ? 4 : (PAIR ? 256 / TILE : MIN_BLOCKS_);
+  // resident CTAs scale with the tile so the register budget per thread stays the natural one
+  static constexpr int MIN_BLOCKS_N = P32 ? 4 : (PAIR ? 256 / NATURAL_TILE : MIN_BLOCKS_);
+  static constexpr int MIN_BLOCKS = (MIN_BLOCKS_N * NATURAL_TILE / TILE) > 0 ? (MIN_BLOCKS_N * NATURAL_TILE / TILE) : 1;
   static constexpr unsigned GEO_TILE_BYTES = TILE * DSG * sizeof(R);
   static constexpr unsigned COEF_TILE_BYTES = TILE * DSC * sizeof(R);
   static constexpr unsigned OUT_A_BYTES = TILE * NA * sizeof(R);

@@ -310,8 +310,9 @@ def _read_device_batch(path, device, dtype=None, chunk_bytes: int = 64 << 20) ->
 
 def _desc_struct(desc: KernelDescriptor, layout: BatchLayout, n: int, base: int, dtype_code: int,
                  geometry: int, coefficients: int, stiffness: int, load: int, error_key: int,
-                 out_layout: BatchLayout | None = None) -> _native.BatchDesc:
-    """C descriptor; ``out_layout`` set -> packed output rows in that layout."""
+                 out_layout: BatchLayout | None = None, tile: int = 0, ctas_per_sm: int = 0) -> _native.BatchDesc:
+    """C descriptor; ``out_layout`` set -> packed output rows in that layout; ``tile`` /
+    ``ctas_per_sm``: the tuner's launch knobs (0 = the kernel's own choice)."""
     d = _native.BatchDesc()
     d.element = _native.ELEMENT[desc.element.value]
     d.problem = _native.PROBLEM[desc.problem.value]
@@ -324,6 +325,7 @@ def _desc_struct(desc: KernelDescriptor, layout: BatchLayout, n: int, base: int,
     d.base_index = base
     d.geometry, d.coefficients = geometry, coefficients
     d.stiffness, d.load, d.error_key = stiffness, load, error_key
+    d.tile_elements, d.ctas_per_sm = int(tile), int(ctas_per_sm)
     if out_layout is None:
         d.out_format, d.out_lane_width = _native.OUT_SPLIT, 1
     else:
@@ -463,7 +465,8 @@ def _check_out(out, batch: DeviceBatch, ns: int, packed: bool):
 
 
 def _integrate_device(desc: KernelDescriptor, batch: DeviceBatch, out_layout, check: bool, base_index: int,
-                      out=None, packed: bool = False, workers: int = 1) -> BatchResult:
+                      out=None, packed: bool = False, workers: int = 1, tile: int = 0,
+                      ctas_per_sm: int = 0) -> BatchResult:
     import torch
 
     lib = _native.load()
@@ -488,7 +491,7 @@ def _integrate_device(desc: KernelDescriptor, batch: DeviceBatch, out_layout, ch
     err = torch.full((1,), -1, dtype=torch.int64, device=dev)
     dd = _desc_struct(desc, batch.layout, n, base_index, dtype_code, batch.geometry_data.data_ptr(),
                       batch.coefficient_data.data_ptr(), ptr_a, ptr_b, err.data_ptr(),
-                      out_layout=olayout if packed else None)
+                      out_layout=olayout if packed else None, tile=tile, ctas_per_sm=ctas_per_sm)
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream().cuda_stream
         if torch.cuda.is_current_stream_capturing():
@@ -553,9 +556,9 @@ def _host_streams(device: int):
 
 
 def host_chunk_elements(n: int) -> int:
-    """Pipeline chunk: ~8+ chunks for big batches, multiple of the 128-element tile."""
+    """Pipeline chunk: ~8+ chunks for big batches, a multiple of 256 elements (every tile size)."""
     chunk = max(16384, min(1 << 19, -(-n // 8)))
-    return -(-chunk // 128) * 128
+    return -(-chunk // 256) * 256
 
 
 _staging: dict[int, np.ndarray] = {}
@@ -593,7 +596,7 @@ def _aligned_f64(a) -> np.ndarray:
 
 
 def _integrate_host(desc: KernelDescriptor, batch, out_layout, base_index: int, packed: bool = False,
-                    workers: int = 1) -> BatchResult:
+                    workers: int = 1, tile: int = 0, ctas_per_sm: int = 0) -> BatchResult:
     import torch
 
     if not torch.cuda.is_available():
@@ -614,7 +617,7 @@ def _integrate_host(desc: KernelDescriptor, batch, out_layout, base_index: int, 
         b = hostmem.empty((n, ns))
         ptr_a, ptr_b = A.ctypes.data, b.ctypes.data
     dd = _desc_struct(desc, layout, n, base_index, _native.DTYPE["float64"], geo.ctypes.data, cof.ctypes.data,
-                      ptr_a, ptr_b, 0, out_layout=olayout if packed else None)
+                      ptr_a, ptr_b, 0, out_layout=olayout if packed else None, tile=tile, ctas_per_sm=ctas_per_sm)
     device = torch.cuda.current_device()
     streams = _host_streams(device)
     chunk = host_chunk_elements(n)
@@ -665,7 +668,8 @@ def _integrate_host(desc: KernelDescriptor, batch, out_layout, base_index: int, 
 # ---------------------------------------------------------------------------
 
 def integrate_batch(desc, batch, out_layout: BatchLayout = ELEMENT_MAJOR, workers: int = 1, *,
-                    check: bool = True, base_index: int = 0, out=None, packed: bool = False) -> BatchResult:
+                    check: bool = True, base_index: int = 0, out=None, packed: bool = False, tile: int = 0,
+                    ctas_per_sm: int = 0) -> BatchResult:
     """Integrate every element of ``batch`` with the kernel named by ``desc``.
 
     Mirrors ``feklab.kernels.integrate_batch`` (``batched.py:536-606``).
@@ -674,26 +678,30 @@ def integrate_batch(desc, batch, out_layout: BatchLayout = ELEMENT_MAJOR, worker
     ``base_index`` offsets reported element indices (sharded batches);
     ``out=(A, b)`` supplies preallocated device outputs; ``packed=True`` has
     the kernel write ``flat_output()``'s packed rows in ``out_layout``
-    directly (``result.flat``; no repacking pass).
+    directly (``result.flat``; no repacking pass); ``tile`` (64/128/256, QSS
+    natural-path descriptors) and ``ctas_per_sm`` are the tuner's launch knobs
+    (0 = the kernel's own choice; results are bitwise independent of both).
     """
     desc = coerce_descriptor(desc)
     _check_match(desc, batch)
     workers = max(1, min(int(workers), int(batch.n_elements)))  # batched.py:569
     if isinstance(batch, DeviceBatch):
-        return _integrate_device(desc, batch, out_layout, check, base_index, out, packed, workers)
+        return _integrate_device(desc, batch, out_layout, check, base_index, out, packed, workers, tile, ctas_per_sm)
     if _is_torch(getattr(batch, "geometry_data", None)):
         raise TypeError("batches of torch tensors must be wrapped in DeviceBatch")
     if out is not None:
         raise TypeError("out= is for device batches (host batches return numpy results)")
-    return _integrate_host(desc, batch, out_layout, base_index, packed, workers)
+    return _integrate_host(desc, batch, out_layout, base_index, packed, workers, tile, ctas_per_sm)
 
 
 
-def launch_config(desc, layout: BatchLayout, n: int, dtype: str = "float64") -> dict:
+def launch_config(desc, layout: BatchLayout, n: int, dtype: str = "float64", tile: int = 0,
+                  ctas_per_sm: int = 0) -> dict:
     """Grid/block/smem/tile that ``fek_integrate`` uses for this case (no launch)."""
     desc = coerce_descriptor(desc)
     lib = _native.load()
-    dd = _desc_struct(desc, coerce_layout(layout), n, 0, _native.DTYPE[dtype], 0, 0, 0, 0, 0)
+    dd = _desc_struct(desc, coerce_layout(layout), n, 0, _native.DTYPE[dtype], 0, 0, 0, 0, 0, tile=tile,
+                      ctas_per_sm=ctas_per_sm)
     g, bl, sm, t = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
     _native.check(lib.fek_launch_config(ctypes.byref(dd), ctypes.byref(g), ctypes.byref(bl), ctypes.byref(sm),
                                         ctypes.byref(t)), "fek_launch_config")

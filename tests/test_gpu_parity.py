@@ -360,3 +360,28 @@ def test_staged_abi_with_pageable_outputs():
     assert rc == 0 and key.value == _native.NO_ERROR
     ref = integrate_batch(desc, ElementBatch.from_arrays(et, pb, geo.reshape(n, -1), cof.reshape(n, -1)))
     assert np.array_equal(A, ref.stiffness) and np.array_equal(b, ref.load)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("et,pb", CASES, ids=lambda c: getattr(c, "value", c))
+def test_tile_and_cta_variants_are_bitwise_identical(et, pb, dtype):
+    """The tuner's launch knobs (tile T = 64/128/256 instantiations, CTAs/SM caps) never change a
+    result: every element runs one instruction sequence whatever the launch shape."""
+    import torch
+
+    from paper_1504_01023_b200 import mesh
+
+    spec = mesh.spec_for_element_count(et, 20_000)
+    geo = mesh.geometry_rows(spec)
+    if et is PRISM:
+        geo = mesh.jitter_top_faces(geo, spec, seed=5)
+    cof = mesh.coefficient_rows(spec.n_elements, pb, et, 5)
+    dev = DeviceBatch.from_host(ElementBatch.from_arrays(et, pb, geo, cof), dtype=getattr(torch, dtype))
+    desc = KernelDescriptor(Variant.QSS, fek.natural_path(et), pb, et)
+    want = integrate_batch(desc, dev)
+    for tile in (64, 128, 256):
+        for ctas in (0, 1, 2):
+            got = integrate_batch(desc, dev, tile=tile, ctas_per_sm=ctas)
+            assert torch.equal(got.stiffness, want.stiffness) and torch.equal(got.load, want.load), (tile, ctas)
+    with pytest.raises(fek.NativeLibraryError):
+        integrate_batch(KernelDescriptor(Variant.SQS, fek.natural_path(et), pb, et), dev, tile=128)

@@ -6,7 +6,7 @@ ROOT=${ROOT:-/root/repo}; CS=$ROOT/paper_1504_01023_b200/csrc; OUT=$ROOT/build/e
 mkdir -p $OUT $ROOT/tools/exp
 for src in $CS/fek_abi.cu $CS/fek_mesh.cu $CS/fek_layout.cu $CS/cases/*.cu; do
   b=$(basename $src .cu)
-  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++20 --fmad=false -Xcompiler -fPIC -I$ROOT/include -DFEK_QSS_ONLY $FLAGS -c $src -o $OUT/$b.o &
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++20 --fmad=false -Xcompiler -fPIC -I$ROOT/include -DFEK_QSS_ONLY -DFEK_NO_TILES $FLAGS -c $src -o $OUT/$b.o &
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static $OUT/*.o -o $ROOT/tools/exp/libfek_$NAME.so
