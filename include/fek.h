@@ -25,6 +25,8 @@
  *                          go into the DegenerateElement/InvertedElement text.
  *   fek_jacobian        <- geometry.py:94-138  jacobian_affine /
  *                          jacobian_at_point (JacobianData) of one element.
+ *   fek_apply           <- (new) the element matrices consumed in
+ *                          the kernel: matrix-free y += sum_e P_e^T A_e P_e x.
  *   fek_checksum        <- (new) per-shard verification sums reduced with
  *                          NCCL across GPUs.
  *
@@ -137,6 +139,21 @@ const char *fek_last_cuda_error(void);
  * Asynchronous: returns after the launch.  Geometry failures are recorded
  * with atomicMin into *d->error_key (the reference's first-error rule). */
 int fek_integrate(const fek_batch_desc *d, void *cuda_stream);
+
+/* Matrix-free operator application fused with the integration (
+ * element contributions used "without assembly, in the so called
+ * matrix-free approaches", the "assembly operation designed as extension of procedures
+ * performing numerical integration").  For every element e of d, with the node numbers
+ * element_nodes[e*ns + s] (int32, ns = 4 / 6):
+ *     y[node(e, r)] += sum_s A_e[r][s] x[node(e, s)]      f[node(e, r)] += b_e[r]
+ * where A_e, b_e are exactly the matrices fek_integrate would write -- the same kernel math,
+ * kept in registers, so A and b never reach memory.  x, y, f (f may be NULL) are device
+ * arrays of d's real type; y and f accumulate with atomicAdd, so the summation order (and
+ * the last bits of y, f) vary between runs.  QSS natural-path descriptors (geo_linear tets,
+ * geo_generic prisms), element-major inputs; d->stiffness / d->load are unused; geometry
+ * errors are reported in d->error_key exactly as by fek_integrate. */
+int fek_apply(const fek_batch_desc *d, const int32_t *element_nodes, const void *x, void *y, void *f,
+              void *cuda_stream);
 
 /* Launch geometry fek_integrate would use (for reporting / launch counting). */
 int fek_launch_config(const fek_batch_desc *d, int *grid, int *block, int *smem_bytes,

@@ -128,9 +128,16 @@ int validate(const fek_batch_desc *d, bool need_pointers) {
   return FEK_OK;
 }
 
+struct ApplyArgs {
+  const int32_t *element_nodes;
+  const void *x;
+  void *y;
+  void *f;
+};
+
 int launch(const fek_batch_desc *d, cudaStream_t stream, int *grid_out, int *block_out, int *smem_out,
-           int *tile_out, bool do_launch) {
-  const int idx = d->tile_elements
+           int *tile_out, bool do_launch, const ApplyArgs *ap = nullptr) {
+  const int idx = ap ? fek::apply_index(d->dtype, d->element, d->problem) : d->tile_elements
                       ? fek::tiled_index(d->dtype, d->element, d->problem,
                                          d->tile_elements == 64 ? 0 : (d->tile_elements == 128 ? 1 : 2))
                       : kernel_index(d->dtype, d->element, d->problem, d->variant, d->geometry_path);
@@ -159,6 +166,10 @@ int launch(const fek_batch_desc *d, cudaStream_t stream, int *grid_out, int *blo
   p.out_packed = d->out_format == FEK_OUT_PACKED;
   p.out_width = p.out_packed ? d->out_lane_width : 1;
   p.scheduler = d->scheduler;
+  p.element_nodes = ap ? ap->element_nodes : nullptr;
+  p.x = ap ? ap->x : nullptr;
+  p.y = ap ? ap->y : nullptr;
+  p.f = ap ? ap->f : nullptr;
   ke.fn<<<grid, ke.threads, ke.smem, stream>>>(p);
   FEK_CUDA(cudaGetLastError());
   return FEK_OK;
@@ -263,6 +274,20 @@ int fek_integrate(const fek_batch_desc *d, void *cuda_stream) {
   if (int rc = validate(d, true)) return rc;
   if (d->n_elements > 0 && !d->error_key) return FEK_ERR_ARGUMENT;
   return launch(d, static_cast<cudaStream_t>(cuda_stream), nullptr, nullptr, nullptr, nullptr, true);
+}
+
+int fek_apply(const fek_batch_desc *d, const int32_t *element_nodes, const void *x, void *y, void *f,
+              void *cuda_stream) {
+  if (int rc = validate(d, false)) return rc;
+  const bool natural = d->variant == FEK_QSS &&
+                       d->geometry_path == (d->element == FEK_TETRAHEDRON ? FEK_GEO_LINEAR : FEK_GEO_GENERIC);
+  if (!natural || d->layout != FEK_ELEMENT_MAJOR || d->tile_elements != 0) return FEK_ERR_ARGUMENT;
+  if (d->n_elements == 0) return FEK_OK;
+  if (!d->geometry || !d->coefficients || !d->error_key || !element_nodes || !x || !y) return FEK_ERR_ARGUMENT;
+  if (!aligned16(d->geometry) || !aligned16(d->coefficients) || reinterpret_cast<uintptr_t>(d->scheduler) % 8)
+    return FEK_ERR_ALIGNMENT;
+  const ApplyArgs ap{element_nodes, x, y, f};
+  return launch(d, static_cast<cudaStream_t>(cuda_stream), nullptr, nullptr, nullptr, nullptr, true, &ap);
 }
 
 int fek_launch_config(const fek_batch_desc *d, int *grid, int *block, int *smem_bytes, int *tile_elements) {

@@ -46,10 +46,39 @@ struct LaunchParams {
   int out_packed;  // FEK_OUT_PACKED: rows [A | b] into `stiffness` in the output layout
   int out_width;   // output lane width (1 = element-major rows)
   unsigned long long *scheduler;  // [next tile, CTAs done] or null (static round-robin)
+  // fused matrix-free apply (Traits APPLY, fek_apply): y[node] += A_e x_e, f[node] += b_e
+  const int *element_nodes;  // (n, NS) int32, element-major
+  const void *x;
+  void *y;
+  void *f;  // may be null
 };
 
+// y[nodes[r]] += sum_s A[r][s] x[nodes[s]] for rows r of one element (RB rows starting at R0 of
+// its A; A_rows holds those rows, NS columns each), f[nodes[r]] += B_rows[r]: fp atomicAdd
+template <typename R, int NS, int ROWS>
+__device__ __forceinline__ void apply_rows(const LaunchParams &p, long long e_local, int r0, const R *A_rows,
+                                           const R *B_rows) {
+  const int *nd = p.element_nodes + e_local * NS;
+  int node[NS];
+  R xs[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) node[s] = __ldg(nd + s);
+#pragma unroll
+  for (int s = 0; s < NS; ++s) xs[s] = __ldg(static_cast<const R *>(p.x) + node[s]);
+  R *y = static_cast<R *>(p.y);
+  R *f = static_cast<R *>(p.f);
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) {
+    R acc = A_rows[NS * r] * xs[0];
+#pragma unroll
+    for (int s = 1; s < NS; ++s) acc = fma(A_rows[NS * r + s], xs[s], acc);
+    atomicAdd(y + node[r0 + r], acc);
+    if (f) atomicAdd(f + node[r0 + r], B_rows[r]);
+  }
+}
+
 // TILE_ = 0: the kernel's own tile; 64 / 128 / 256: the tuner's tile-size variants (fek_dispatch.cuh)
-template <typename R_, int ET_, int PB_, int VAR_, int GEO_, int TILE_ = 0>
+template <typename R_, int ET_, int PB_, int VAR_, int GEO_, int TILE_ = 0, bool APPLY_ = false>
 struct Traits {
   using R = R_;
   static constexpr int ET = ET_, PB = PB_, VAR = VAR_, GEO = GEO_;
@@ -70,6 +99,8 @@ struct Traits {
                                VAR == QSS && sizeof(R) == 8;
   static constexpr int NATURAL_TILE = PAIR ? FEK_PAIR_TILE : 128;
   static constexpr int TILE = TILE_ ? TILE_ : NATURAL_TILE;  // elements per tile (a multiple of every lane width)
+  // fused matrix-free apply: A and b stay in registers, no output tile, no bulk stores
+  static constexpr bool APPLY = APPLY_;
   static_assert(TILE % 64 == 0, "a tile must be a whole number of lane blocks for every lane width");
   static constexpr int LANES = PAIR ? 2 : 1;
   static constexpr int THREADS = TILE * LANES;
@@ -105,8 +136,8 @@ struct Traits {
   static constexpr int MIN_BLOCKS = (MIN_BLOCKS_N * NATURAL_TILE / TILE) > 0 ? (MIN_BLOCKS_N * NATURAL_TILE / TILE) : 1;
   static constexpr unsigned GEO_TILE_BYTES = TILE * DSG * sizeof(R);
   static constexpr unsigned COEF_TILE_BYTES = TILE * DSC * sizeof(R);
-  static constexpr unsigned OUT_A_BYTES = TILE * NA * sizeof(R);
-  static constexpr unsigned OUT_B_BYTES = TILE * NS * sizeof(R);
+  static constexpr unsigned OUT_A_BYTES = APPLY ? 0u : TILE * NA * sizeof(R);
+  static constexpr unsigned OUT_B_BYTES = APPLY ? 0u : TILE * NS * sizeof(R);
   static constexpr unsigned GEO_OFFSET = 0;
   static constexpr unsigned COEF_OFFSET = STAGES * GEO_TILE_BYTES;
   static constexpr unsigned OUT_A_OFFSET = COEF_OFFSET + STAGES * COEF_TILE_BYTES;
@@ -256,6 +287,10 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
         prism_pair::integrate_cd_level(J2, J01, C, bound, z, Ah, Bh, kind, kind_point);
       }
       if (act && z == 0 && kind) atomicMin(p.error_key, make_error_key(p.base + e0 + el, kind_point, kind));
+      if constexpr (K::APPLY) {
+        if (act) apply_rows<R, 6, 3>(p, e0 + el, 3 * z, Ah, Bh);  // lane z: rows a + 3z
+        continue;
+      }
       constexpr unsigned RB = sizeof(R);
       if (p.out_packed) {
         constexpr int DSO = 42;
@@ -354,6 +389,10 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
       if (!release()) break;
     }
     if (kind) atomicMin(p.error_key, make_error_key(e_abs, kind_point, kind));
+    if constexpr (K::APPLY) {
+      if (active) apply_rows<R, K::NS, K::NS>(p, e0 + tid, 0, A, B);
+      continue;
+    }
     if (tid == 0) bulk_wait_read<0>();
     __syncthreads();
     if (p.out_packed) {

@@ -1,0 +1,81 @@
+"""Matrix-free operator application fused with the integration.
+
+    y, f = apply_batch(desc, device_batch, element_nodes, x)      # y += A x, f += b (assembled)
+
+The paper stops at the element matrices and leaves their use open: assembly, or "without
+assembly, in the so called matrix-free approaches", the output possibly kept
+"in registers if e.g. assembly operation is designed as extension of procedures performing
+numerical integration".  ``fek_apply`` is that extension: the integration
+kernel's A_e and b_e stay in registers and are consumed in place,
+
+    y[node(e, r)] += sum_s A_e[r][s] x[node(e, s)],      f[node(e, r)] += b_e[r],
+
+so a Krylov solver's operator application costs one pass over the element inputs (plus the
+connectivity and the gathered x) instead of integrate -> store 36 + 6 reals per element ->
+read them back.  The sums use atomicAdd, so the order in which element contributions land --
+and the last bits of y and f -- vary between runs; A_e and b_e themselves are bitwise the ones
+``integrate_batch`` returns.  There is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from .. import _native
+from ..errors import NativeLibraryError
+from ..layout import ELEMENT_MAJOR
+from ..problems import coerce_descriptor
+from .batched import DeviceBatch, _check_match, _desc_struct, _raise_geometry, _device_error_detail, \
+    _tile_queue, resolve_error_key
+
+
+def apply_batch(desc, batch: DeviceBatch, element_nodes, x, y=None, f=None, *, check: bool = True,
+                base_index: int = 0):
+    """y += sum_e P_e^T A_e P_e x and f += sum_e P_e^T b_e for a device batch; returns (y, f).
+
+    ``element_nodes``: (n, ns) int32 CUDA tensor of global node numbers (``mesh.element_nodes``);
+    ``x``: CUDA vector of the batch's dtype indexed by node; ``y`` / ``f``: accumulators (zeros of
+    x's shape when None; pass ``f=False`` to skip the load assembly).  The batch must be
+    element-major and the descriptor a QSS natural-path one (geo_linear tets, geo_generic prisms).
+    Geometry errors raise exactly as ``integrate_batch``'s.
+    """
+    import torch
+
+    desc = coerce_descriptor(desc)
+    _check_match(desc, batch)
+    if not isinstance(batch, DeviceBatch):
+        raise TypeError("apply_batch takes a DeviceBatch (inputs in HBM)")
+    if batch.layout != ELEMENT_MAJOR:
+        raise ValueError("apply_batch needs an element-major batch (DeviceBatch.convert(ELEMENT_MAJOR))")
+    n, ns = batch.n_elements, desc.element.n_shape
+    dev = batch.geometry_data.device
+    if not (isinstance(element_nodes, torch.Tensor) and element_nodes.is_cuda and element_nodes.dtype == torch.int32
+            and tuple(element_nodes.shape) == (n, ns) and element_nodes.is_contiguous()):
+        raise ValueError(f"element_nodes must be a contiguous ({n}, {ns}) int32 CUDA tensor")
+    for name, t in (("x", x),) + (() if y is None else (("y", y),)) + (() if f is None or f is False else (("f", f),)):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == batch.dtype and t.dim() == 1
+                and t.is_contiguous() and t.device == dev):
+            raise ValueError(f"{name} must be a contiguous 1-D CUDA tensor of the batch's dtype on {dev}")
+    if y is None:
+        y = torch.zeros_like(x)
+    if f is None:
+        f = torch.zeros_like(x)
+    lib = _native.load()
+    dtype_code = _native.DTYPE["float64" if batch.dtype == torch.float64 else "float32"]
+    err = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    dd = _desc_struct(desc, ELEMENT_MAJOR, n, base_index, dtype_code, batch.geometry_data.data_ptr(),
+                      batch.coefficient_data.data_ptr(), 0, 0, err.data_ptr())
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream().cuda_stream
+        dd.scheduler = _tile_queue(dev, stream).data_ptr()
+        rc = lib.fek_apply(ctypes.byref(dd), element_nodes.data_ptr(), x.data_ptr(), y.data_ptr(),
+                           None if f is False else f.data_ptr(), stream)
+        if rc == _native.ERR_ARGUMENT:
+            raise NativeLibraryError(f"fek_apply: {desc.short_name()} is not a QSS natural-path descriptor "
+                                     "or the batch is not element-major")
+        _native.check(rc, "fek_apply")
+        if check:
+            key = resolve_error_key(dd, err, stream)
+            if key != _native.NO_ERROR:
+                _raise_geometry(key, lambda e, q: _device_error_detail(dd, e - base_index, q, stream))
+    return y, (None if f is False else f)

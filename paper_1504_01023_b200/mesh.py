@@ -101,6 +101,50 @@ def _prism_rows(spec: MeshSpec, cells: slice | None = None) -> np.ndarray:
     return rows.reshape(-1, 18)
 
 
+def node_count(spec: MeshSpec) -> int:
+    """Vertices of the structured unit-cube mesh: (nx+1)(ny+1)(nz+1) grid points (tets) or the
+    (nx+1)(ny+1) base points at z = 0 and z = 1 (prisms)."""
+    if spec.element_type is ElementType.TETRAHEDRON:
+        return (spec.nx + 1) * (spec.ny + 1) * (spec.nz + 1)
+    return (spec.nx + 1) * (spec.ny + 1) * 2
+
+
+def element_nodes(spec: MeshSpec) -> np.ndarray:
+    """(n, nv) int32 global node numbers of every element, in geometry_rows' element and vertex
+    order: the connectivity a matrix-free apply scatters through (kernels/apply.py).  The
+    reference's batches carry coordinates only; for its structured meshes the topology is the
+    grid's -- tets: the Kuhn path from the cell origin, prisms: the two base triangles extruded.
+    (Top-face jitter moves coordinates, not connectivity.)"""
+    if spec.element_type is ElementType.TETRAHEDRON:
+        nx, ny, nz = spec.nx, spec.ny, spec.nz
+        cell = np.arange(nx * ny * nz, dtype=np.int64)
+        ix, rem = np.divmod(cell, ny * nz)
+        iy, iz = np.divmod(rem, nz)
+        out = np.empty((cell.size, 6, 4), dtype=np.int64)
+        node = lambda dx, dy, dz: ((ix + dx) * (ny + 1) + (iy + dy)) * (nz + 1) + (iz + dz)  # noqa: E731
+        for p, (perm, odd) in enumerate(zip(_PERMS, _ODD)):
+            step = [0, 0, 0]
+            verts = [node(0, 0, 0)]
+            for axis in perm:
+                step[axis] = 1
+                verts.append(node(*step))
+            if odd:
+                verts[1], verts[2] = verts[2], verts[1]
+            out[:, p] = np.stack(verts, axis=1)
+        return out.reshape(-1, 4).astype(np.int32)
+    nx, ny = spec.nx, spec.ny
+    cell = np.arange(nx * ny, dtype=np.int64)
+    ix, iy = np.divmod(cell, ny)
+    base = lambda dx, dy: ((ix + dx) * (ny + 1) + (iy + dy)) * 2  # noqa: E731
+    tris = (((0, 0), (1, 0), (0, 1)), ((1, 0), (1, 1), (0, 1)))
+    out = np.empty((cell.size, 2, 6), dtype=np.int64)
+    for t, tri in enumerate(tris):
+        for v, (dx, dy) in enumerate(tri):
+            out[:, t, v] = base(dx, dy)
+            out[:, t, v + 3] = base(dx, dy) + 1
+    return out.reshape(-1, 6).astype(np.int32)
+
+
 def geometry_rows(spec: MeshSpec) -> np.ndarray:
     if spec.element_type is ElementType.TETRAHEDRON:
         return _tet_rows(spec)

@@ -1,0 +1,96 @@
+"""Fused matrix-free apply (fek_apply, kernels/apply.py) against the oracle and the two-pass path.
+
+y = sum_e P_e^T A_e P_e x and f = sum_e P_e^T b_e, with A_e, b_e kept in the integration kernel's
+registers.  The element matrices are the reference's (oracle: bitwise-pinned numpy restatement);
+only the order of the atomicAdd accumulation differs, so entries are compared relative to the
+sum of the magnitudes of their contributions (<= 1e-13).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1504_01023_b200 as fek
+from oracle import numpy_oracle as O
+from paper_1504_01023_b200 import DeviceBatch, ElementBatch, ElementType, KernelDescriptor, ProblemClass, Variant, mesh
+
+pytestmark = pytest.mark.gpu
+
+CASES = [(ElementType.TETRAHEDRON, ProblemClass.CONV_DIFF, mesh.MeshSpec(12, 10, 9, ElementType.TETRAHEDRON)),
+         (ElementType.TETRAHEDRON, ProblemClass.POISSON, mesh.MeshSpec(9, 8, 7, ElementType.TETRAHEDRON)),
+         (ElementType.PRISM, ProblemClass.CONV_DIFF, mesh.MeshSpec(101, 77, 1, ElementType.PRISM)),
+         (ElementType.PRISM, ProblemClass.POISSON, mesh.MeshSpec(61, 53, 1, ElementType.PRISM))]
+
+
+def _setup(et, pb, spec, seed=3):
+    geo = mesh.geometry_rows(spec)
+    if et is ElementType.PRISM:
+        geo = mesh.jitter_top_faces(geo, spec, seed=seed)
+    cof = mesh.coefficient_rows(spec.n_elements, pb, et, seed)
+    nodes = mesh.element_nodes(spec)
+    x = np.random.default_rng(seed).uniform(-1, 1, mesh.node_count(spec))
+    return geo, cof, nodes, x
+
+
+def _scatter(A, b, nodes, x, n_nodes):
+    xe = x[nodes]                                       # (n, ns)
+    ye = np.einsum("ers,es->er", A, xe)
+    mag = np.einsum("ers,es->er", np.abs(A), np.abs(xe))
+    y, f, ym, fm = (np.zeros(n_nodes) for _ in range(4))
+    np.add.at(y, nodes, ye)
+    np.add.at(ym, nodes, mag)
+    np.add.at(f, nodes, b)
+    np.add.at(fm, nodes, np.abs(b))
+    return y, f, ym, fm
+
+
+@pytest.mark.parametrize("et,pb,spec", CASES, ids=lambda c: getattr(c, "value", None) or str(getattr(c, "nx", c)))
+def test_apply_matches_oracle(et, pb, spec):
+    geo, cof, nodes, x = _setup(et, pb, spec)
+    desc = KernelDescriptor(Variant.QSS, fek.natural_path(et), pb, et)
+    A, b = O.integrate("qss", desc.geometry_path.value, pb.value, et.value, geo, cof)
+    y_ref, f_ref, ym, fm = _scatter(A, b, nodes, x, len(x))
+    dev = DeviceBatch.from_host(ElementBatch.from_arrays(et, pb, geo, cof))
+    y, f = fek.apply_batch(desc, dev, torch.from_numpy(nodes).cuda(), torch.from_numpy(x).cuda())
+    y, f = y.cpu().numpy(), f.cpu().numpy()
+    assert (np.abs(y - y_ref) <= 1e-13 * ym + 1e-300).all()
+    assert (np.abs(f - f_ref) <= 1e-13 * fm + 1e-300).all()
+
+
+def test_apply_equals_two_pass_at_c4_size():
+    """C4 (16M jittered prisms, ConvDiff): fused apply vs integrate_batch -> stored A, b -> scatter."""
+    cfg = mesh.bench_configs()["C4"]
+    geo, cof = mesh.device_config(cfg)
+    et, pb = cfg.spec.element_type, cfg.problem
+    n = cfg.spec.n_elements
+    dev = DeviceBatch(et, pb, n, fek.ELEMENT_MAJOR, geo, cof)
+    nodes = torch.from_numpy(mesh.element_nodes(cfg.spec)).cuda()
+    x = torch.rand(mesh.node_count(cfg.spec), dtype=torch.float64, device="cuda", generator=torch.Generator(
+        device="cuda").manual_seed(7)) * 2 - 1
+    desc = KernelDescriptor(Variant.QSS, fek.natural_path(et), pb, et)
+    y, f = fek.apply_batch(desc, dev, nodes, x)
+    res = fek.integrate_batch(desc, dev)
+    idx = nodes.long()
+    xe = x[idx]
+    ye = torch.einsum("ers,es->er", res.stiffness, xe)
+    mag = torch.einsum("ers,es->er", res.stiffness.abs(), xe.abs())
+    y2, ym, f2, fm = (torch.zeros_like(x) for _ in range(4))
+    y2.index_add_(0, idx.reshape(-1), ye.reshape(-1))
+    ym.index_add_(0, idx.reshape(-1), mag.reshape(-1))
+    f2.index_add_(0, idx.reshape(-1), res.load.reshape(-1))
+    fm.index_add_(0, idx.reshape(-1), res.load.abs().reshape(-1))
+    assert bool(((y - y2).abs() <= 1e-13 * ym).all()) and bool(((f - f2).abs() <= 1e-13 * fm).all())
+
+
+def test_apply_reports_geometry_errors_like_integrate_batch():
+    et, pb, spec = CASES[2]
+    geo, cof, nodes, x = _setup(et, pb, spec)
+    geo[1234] = -geo[1234]
+    dev = DeviceBatch.from_host(ElementBatch.from_arrays(et, pb, geo, cof))
+    desc = KernelDescriptor(Variant.QSS, fek.natural_path(et), pb, et)
+    with pytest.raises(fek.InvertedElement) as err:
+        fek.apply_batch(desc, dev, torch.from_numpy(nodes).cuda(), torch.from_numpy(x).cuda())
+    assert (err.value.element_index, err.value.point_index) == (1234, 0)
+    with pytest.raises(fek.NativeLibraryError):
+        fek.apply_batch(KernelDescriptor(Variant.SQS, fek.natural_path(et), pb, et), dev,
+                        torch.from_numpy(nodes).cuda(), torch.from_numpy(x).cuda())

@@ -173,3 +173,28 @@ def test_bench_inputs_equal_reference_generator(key):
     assert geo.shape[0] == int(z["n_elements"][0])
     assert np.array_equal(geo[z["index"]], z["geometry_rows"])
     assert np.array_equal(cof[z["index"]], z["coefficient_rows"])
+
+
+@pytest.mark.parametrize("et", [ElementType.TETRAHEDRON, ElementType.PRISM])
+def test_element_nodes_are_consistent_with_the_geometry(et):
+    """mesh.element_nodes: one coordinate per node number across all elements, every node used."""
+    from paper_1504_01023_b200 import mesh
+
+    spec = mesh.MeshSpec(4, 3, 5, et) if et is ElementType.TETRAHEDRON else mesh.MeshSpec(7, 5, 1, et)
+    nodes = mesh.element_nodes(spec)
+    geo = mesh.geometry_rows(spec).reshape(len(nodes), -1, 3)
+    assert nodes.dtype == np.int32 and nodes.shape == (spec.n_elements, et.n_vertices)
+    coords = np.full((mesh.node_count(spec), 3), np.nan)
+    coords[nodes.reshape(-1)] = geo.reshape(-1, 3)
+    # (a node reached from different cells differs by rounding only: x0 + h vs (i + 1) h)
+    assert np.allclose(coords[nodes], geo, rtol=0, atol=1e-14) and not np.isnan(coords).any()
+
+
+def test_config_window_is_the_prefix_of_the_full_configuration():
+    from paper_1504_01023_b200 import mesh
+
+    for key in ("C1", "C3"):
+        cfg = mesh.bench_configs()[key]
+        g, c = mesh.config_rows(cfg)
+        gw, cw = mesh.config_window(cfg, 50_001)
+        assert np.array_equal(g[:50_001], gw) and np.array_equal(c[:50_001], cw)
