@@ -61,7 +61,7 @@ def parse(argv=None):
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", default="C5")
-    ap.add_argument("--cases", default="C1,C2,C3,C4,C4f32,C2packed",
+    ap.add_argument("--cases", default="C1,C2,C3,C4,C4f32,C2packed,C4apply",
                     help="extra per-config kernel timings (N=1 only)")
     ap.add_argument("--no-cases", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -440,6 +440,82 @@ def c5_parts(world: int, rank: int):
     return parts
 
 
+def measure_apply(key: str, steps: int, warmup: int):
+    """The fused matrix-free apply (fek_apply) on a configuration vs the two-pass alternative.
+
+    Fused: one kernel per step reads the element inputs, the connectivity and the gathered x and
+    scatters y += A_e x_e, f += b_e by atomicAdd (A_e, b_e never leave registers).  Two-pass: the
+    integration kernel stores A and b (the `cases` timing), then a torch gather + batched matvec +
+    index_add scatter reads them back.  Both CUDA-graph timed over `steps` steps.
+    """
+    import torch
+
+    from paper_1504_01023_b200 import ELEMENT_MAJOR, KernelDescriptor, _native, mesh, natural_path
+    from paper_1504_01023_b200.kernels.batched import _desc_struct
+    from paper_1504_01023_b200.measure import hbm_peak
+    from paper_1504_01023_b200.problems import Variant
+
+    cfg = mesh.bench_configs()[key]
+    et, pb = cfg.spec.element_type, cfg.problem
+    n = cfg.spec.n_elements
+    desc = KernelDescriptor(Variant.QSS, natural_path(et), pb, et)
+    geo, cof = mesh.device_config(cfg)
+    nodes = torch.from_numpy(mesh.element_nodes(cfg.spec)).cuda()
+    nn = mesh.node_count(cfg.spec)
+    x = torch.rand(nn, dtype=torch.float64, device="cuda")
+    y, f = torch.zeros_like(x), torch.zeros_like(x)
+    err = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    sched = torch.zeros(2, dtype=torch.int64, device="cuda")
+    dd = _desc_struct(desc, ELEMENT_MAJOR, n, 0, 0, geo.data_ptr(), cof.data_ptr(), 0, 0, err.data_ptr())
+    dd.scheduler = sched.data_ptr()
+    lib = _native.load()
+
+    class Apply:
+        stream = torch.cuda.current_stream().cuda_stream
+
+        def __call__(self):
+            _native.check(lib.fek_apply(ctypes.byref(dd), nodes.data_ptr(), x.data_ptr(), y.data_ptr(),
+                                        f.data_ptr(), self.stream), "fek_apply")
+
+    fused_ms = time_graph([Apply()], steps, warmup) / steps
+    if int(err.item()) != -1:
+        raise RuntimeError(f"{key} apply: geometry error key {int(err.item()) & 0xFFFFFFFFFFFFFFFF:#x}")
+    L = Launcher(desc, geo, cof)
+    idx = nodes.long()
+    flat = idx.reshape(-1)
+
+    def two_pass():
+        L()
+        xe = x[idx]
+        ye = torch.bmm(L.A, xe.unsqueeze(2)).squeeze(2)
+        y.index_add_(0, flat, ye.reshape(-1))
+        f.index_add_(0, flat, L.b.reshape(-1))
+
+    two_pass.launchers = [L]
+    torch.cuda.synchronize()
+    two_ms = time_graph([two_pass], steps, warmup) / steps
+    integrate_ms = time_graph([L], steps, warmup) / steps
+    rb = 8
+    hbm = hbm_peak()[0]
+    ns = et.n_shape
+    fused_bytes = n * (et.geometry_size + pb.coefficient_size(et)) * rb + n * ns * 4
+    # the best any two-pass scheme can do: this integration launch storing A, b, then reading them
+    # (and the connectivity) back at the full copy bandwidth
+    reread = n * (ns * ns + ns) * rb + n * ns * 4
+    two_pass_floor_ms = integrate_ms + reread / (hbm * 1e9) * 1e3
+    rec = {"workload": f"{cfg.text}: y += sum_e A_e x_e, f += sum_e b_e (matrix-free, fp64)", "elements": n,
+           "nodes": nn, "descriptor": desc.short_name(), "fused_ms": fused_ms, "fused_value": n / (fused_ms / 1e3),
+           "unit": UNIT, "integrate_store_ms": integrate_ms, "two_pass_floor_ms": two_pass_floor_ms,
+           "speedup_vs_two_pass_floor": two_pass_floor_ms / fused_ms, "two_pass_torch_ms": two_ms,
+           "fused_stream_bytes_per_launch": fused_bytes,
+           "note": "fused: element inputs + int32 connectivity streamed, A and b never stored; x gathers and "
+                   "y/f atomicAdds hit L2.  two_pass_floor = the integration launch storing A, b + re-reading "
+                   "them at the copy peak; two_pass_torch = that launch + torch gather / bmm / index_add"}
+    del L, geo, cof, nodes
+    torch.cuda.empty_cache()
+    return rec
+
+
 def load_profile_traffic(kernel_tag: str, n: int):
     """DRAM bytes of one launch over n elements: the committed ncu capture's bytes per element x n."""
     rec = load_profile_record(kernel_tag)
@@ -757,7 +833,8 @@ def run_c5(args) -> int:
         cases = {}
         for key in [c for c in args.cases.split(",") if c]:
             try:
-                cases[key] = measure_case(key, args.steps, args.warmup)
+                cases[key] = measure_apply(key[:-5], args.steps, args.warmup) if key.endswith("apply") else \
+                    measure_case(key, args.steps, args.warmup)
             except Exception as exc:  # keep the headline line even if a case fails
                 cases[key] = {"error": f"{type(exc).__name__}: {exc}"}
         out["cases"] = cases
@@ -920,7 +997,8 @@ def run_ours(args) -> int:
         cases = {}
         for key in [c for c in args.cases.split(",") if c]:
             try:
-                cases[key] = measure_case(key, args.steps, args.warmup)
+                cases[key] = measure_apply(key[:-5], args.steps, args.warmup) if key.endswith("apply") else \
+                    measure_case(key, args.steps, args.warmup)
             except Exception as exc:  # keep the headline line even if a case fails
                 cases[key] = {"error": f"{type(exc).__name__}: {exc}"}
         out["cases"] = cases
