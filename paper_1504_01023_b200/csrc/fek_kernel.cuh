@@ -216,6 +216,8 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
   // records each stage's tile in smem before arriving on the stage barrier, so
   // consumers read it after the wait; tiles past the end arrive without bytes.
   __shared__ long long s_tile[K::STAGES];
+  __shared__ unsigned s_out_done;  // PAIR: warps done writing the output tile (the last one stores it)
+  if (tid == 0) s_out_done = 0;
   long long static_next = blockIdx.x;
   auto issue_stage = [&](int s) {
     long long t;
@@ -281,8 +283,10 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
         // the previous tile's bulk stores have read the output tile by now (they left before
         // this tile's prologue): checked before the release barrier, which then also frees the
         // output tile -- two CTA barriers per tile instead of three (C4 2.020 -> 2.004 ms).
-        // Per-warp output stores (no CTA barrier before them) measured slower: 2.028 ms.
-        if (tid == 0) bulk_wait_read<0>();
+        // Per-warp output stores (no CTA barrier before them) measured slower: 2.028 ms.  The
+        // split-format store is issued by whichever warp finishes the tile last, so every warp's
+        // lane 0 waits on its own (possibly empty) bulk groups here.
+        if ((tid & 31) == 0) bulk_wait_read<0>();
         if (!release()) break;
         prism_pair::integrate_cd_level(J2, J01, C, bound, z, Ah, Bh, kind, kind_point);
       }
@@ -331,12 +335,20 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
 #pragma unroll
         for (int j = 0; j < 3; ++j) sts64(out_b + static_cast<uint32_t>(el) * 6u * RB + 24u * z + 8u * j, pack1(Bh[j]));
       }
+      // no CTA barrier: the last warp to finish its rows stores the whole tile (one bulk store
+      // pair per tile, as before, without the others waiting for the slowest warp)
       fence_proxy_async_smem();
-      __syncthreads();
-      if (tid == 0) {  // fp64 rows of 288 / 48 bytes: multiples of 16
-        bulk_store(static_cast<char *>(p.stiffness) + e0 * K::NA * RB, out_a, count * K::NA * RB);
-        bulk_store(static_cast<char *>(p.load) + e0 * K::NS * RB, out_b, count * K::NS * RB);
-        bulk_commit();
+      __syncwarp();
+      if ((tid & 31) == 0) {
+        __threadfence_block();
+        if (atomicAdd(&s_out_done, 1u) == K::THREADS / 32 - 1) {
+          __threadfence_block();
+          s_out_done = 0;  // next tile's arrivals come after the next release barrier
+          // fp64 rows of 288 / 48 bytes: multiples of 16
+          bulk_store(static_cast<char *>(p.stiffness) + e0 * K::NA * RB, out_a, count * K::NA * RB);
+          bulk_store(static_cast<char *>(p.load) + e0 * K::NS * RB, out_b, count * K::NS * RB);
+          bulk_commit();
+        }
       }
       continue;
     }
@@ -443,6 +455,9 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
       for (unsigned k = ab16; k < ab; k += 4) *reinterpret_cast<uint32_t *>(ga + k) = lds32(out_a + k);
       for (unsigned k = bb16; k < bb; k += 4) *reinterpret_cast<uint32_t *>(gb + k) = lds32(out_b + k);
     }
+  }
+  if constexpr (K::PAIR) {
+    if ((tid & 31) == 0) bulk_wait_all<0>();  // the last-arriving warp's stores
   }
   if (tid == 0) {
     bulk_wait_all<0>();  // no bulk store may still be reading smem at exit
