@@ -385,3 +385,31 @@ def test_tile_and_cta_variants_are_bitwise_identical(et, pb, dtype):
             assert torch.equal(got.stiffness, want.stiffness) and torch.equal(got.load, want.load), (tile, ctas)
     with pytest.raises(fek.NativeLibraryError):
         integrate_batch(KernelDescriptor(Variant.SQS, fek.natural_path(et), pb, et), dev, tile=128)
+
+
+def test_out_arrays_are_validated_before_the_launch():
+    """integrate_batch(..., out=(A, b)) rejects wrong dtype / shape / device / strides / alignment
+    instead of letting the kernel write through raw pointers."""
+    import torch
+
+    z, host = corpus(PRISM, CONVDIFF)
+    dev = DeviceBatch.from_host(host)
+    n = dev.n_elements
+    desc = KernelDescriptor(Variant.QSS, GeometryPath.GEO_GENERIC, CONVDIFF, PRISM)
+    ok = (torch.empty((n, 6, 6), dtype=torch.float64, device="cuda"), torch.empty((n, 6), dtype=torch.float64,
+                                                                                    device="cuda"))
+    integrate_batch(desc, dev, out=ok)
+    bad = [
+        (torch.empty((n, 6, 6), dtype=torch.float32, device="cuda"), ok[1]),          # dtype
+        (torch.empty((n - 1, 6, 6), dtype=torch.float64, device="cuda"), ok[1]),      # shape
+        (ok[0], torch.empty((n, 6), dtype=torch.float64)),                            # host tensor
+        (torch.empty((n, 6, 12), dtype=torch.float64, device="cuda")[:, :, :6], ok[1]),  # strided
+        (torch.empty(n * 36 + 1, dtype=torch.float64, device="cuda")[1:].view(n, 6, 6), ok[1]),  # misaligned
+    ]
+    for out in bad:
+        with pytest.raises((TypeError, ValueError)):
+            integrate_batch(desc, dev, out=out)
+    with pytest.raises(ValueError):
+        integrate_batch(desc, dev, out=ok, packed=True)
+    with pytest.raises(TypeError):
+        integrate_batch(desc, host, out=ok)
