@@ -9,5 +9,5 @@ grep -h '^{' gpurun_out/bench.log > gpurun_out/bench_line.json
 grep -h '^{' gpurun_out/bench_ref.log > gpurun_out/bench_ref_line.json
 # launch list of the bench command (graph-timed steps included), only after it ran clean without ncu
 python bench.py --steps 5 --warmup 3 --no-cases --no-cpu --no-e2e > gpurun_out/bench_small.log 2>&1 && \
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r01.csv \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG:-r02}.csv \
   python bench.py --steps 5 --warmup 3 --no-cases --no-cpu --no-e2e > gpurun_out/ncu_launches.log 2>&1; echo launches=$?
