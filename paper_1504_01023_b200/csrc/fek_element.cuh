@@ -1104,9 +1104,12 @@ __device__ __forceinline__ R axpy_exact(Cf &&C, Xf &&x) {
 }
 
 // The pair's shared geometry, split between the two lanes (both lanes end with all of it):
-//  * bound = NEAR_TOL_FACTOR * 1e-14 * diag^3 (batched.py:136-148): lane z takes the min/max of
-//    coordinate dimension z, both take dimension 2; the partner's span^2 arrives by shuffle and
-//    the sum keeps the reference's order (s0 + s1) + s2;
+//  * bound2, the SQUARED near bound: (NEAR_TOL_FACTOR 1e-14)^2 D2^3 with D2 = 4 sum_v |X_v - X_0|^2.
+//    The near test only needs a bound >= 1.4 tol (classify_fast: |det - det_ref| <= 0.4 tol), and
+//    span_i <= 2 max_v |X_v,i - X_0,i| gives D2 >= diag^2, so this is >= (16 tol)^2 -- no min/max
+//    (DSETP + 2 FSEL each), no sqrt, no cube: lane z sums coordinate dimension z over the five
+//    vertices plus dimension 2 over vertices {1,2,3} (z = 0) or {4,5} (z = 1), one shuffle adds
+//    the halves.  (Valid elements have det^2 ~ 1e26 bound2, so it never flags them.)
 //  * J2[t][i] = sum_v ld[2t][v][2] X[v][i] (coefficients -+lam_a(t)/2, never 0 or +-1): lane z
 //    forms triangle point t = z and J2[2][z], both form J2[2][2], the other four arrive by shuffle;
 //  * this level's J01[i][k] = sum_v ld[z][v][k] X[v][i]: the level coefficients +-l_b(z) differ
@@ -1114,23 +1117,26 @@ __device__ __forceinline__ R axpy_exact(Cf &&C, Xf &&x) {
 // All entries are bitwise the reference's (jac_entry<PRISM, q, k> / degeneracy_tolerance).
 template <typename R>
 __device__ __forceinline__ void level_geometry(const R (&X)[18], int z, R &bound, R (&J2)[3][3], R (&J01)[3][2]) {
+  // (`bound` receives the squared near bound, bound2)
   constexpr unsigned FULL = 0xffffffffu;
-  // -- bounding box
-  auto span2 = [&](auto pick) {
-    R hi = pick(0), lo = pick(0);
+  // -- squared near bound
+  R part = R(0);
+  {
+    const R x0 = z ? X[1] : X[0];
 #pragma unroll
     for (int v = 1; v < 6; ++v) {
-      hi = fmax(hi, pick(v));
-      lo = fmin(lo, pick(v));
+      const R d = (z ? X[3 * v + 1] : X[3 * v]) - x0;
+      part = fma(d, d, part);
     }
-    const R sp = hi - lo;
-    return sp * sp;
-  };
-  const R mine = span2([&](int v) { return z ? X[3 * v + 1] : X[3 * v]; });  // dimension z
-  const R s2 = span2([&](int v) { return X[3 * v + 2]; });
-  const R theirs = __shfl_xor_sync(FULL, mine, 1);
-  const R s0 = z ? theirs : mine, s1 = z ? mine : theirs;
-  bound = R(NEAR_TOL_FACTOR) * (R(1e-14) * cube_rn(sqrt((s0 + s1) + s2)));
+    // dimension 2: vertices 1, 2, 3 on lane 0; 4, 5 (and vertex 0 itself, d = 0) on lane 1
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const R d = (z ? X[3 * (k == 2 ? 0 : 4 + k) + 2] : X[3 * (1 + k) + 2]) - X[2];
+      part = fma(d, d, part);
+    }
+  }
+  const R d2 = R(4) * (part + __shfl_xor_sync(FULL, part, 1));
+  bound = R(NEAR_TOL_FACTOR * NEAR_TOL_FACTOR * 1e-28) * ((d2 * d2) * d2);
   // -- zeta column at the triangle points
   R own[3];  // J2[z][i]
 #pragma unroll
@@ -1184,7 +1190,7 @@ static_assert(S::ld(2, 0, 2) != 0.0 && S::ld(0, 0, 2) != 0.0 && S::ld(4, 0, 2) !
 
 template <typename R>
 __device__ __forceinline__ void integrate_cd_level(const R (&J2)[3][3], const R (&J01)[3][2], const R (&c)[20],
-                                                   R bound, int z, R (&Ah)[18], R (&Bh)[3], int &kind,
+                                                   R bound2, int z, R (&Ah)[18], R (&Bh)[3], int &kind,
                                                    int &kind_point) {
   using prism_ref::mac;
   using prism_ref::xdot;
@@ -1203,7 +1209,8 @@ __device__ __forceinline__ void integrate_cd_level(const R (&J2)[3][3], const R 
     const R Jt[3] = {J2[t][0], J2[t][1], J2[t][2]};
     R adj[3][3];
     const R det = prism_ref::adjugate(J01, Jt, adj);
-    fail_mask |= prism_ref::kind_bits(det, bound, 2 * t + z, near_mask);
+    near_mask |= static_cast<unsigned>(det * det <= bound2) << (2 * t + z);  // squared near bound
+    fail_mask |= static_cast<unsigned>(det < R(0)) << (2 * t + z);
     const R rdet = R(w) * recip(det);
     R K[4][4];
     K[0][0] = det * wc00;
