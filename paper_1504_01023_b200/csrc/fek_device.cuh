@@ -315,6 +315,31 @@ struct RowIO {
     }
   }
 
+  // element-major row in natural chunk order, no rotation: for the lane-pair kernel, where a
+  // quarter-warp phase touches 4 distinct rows (the two lanes of a pair read the same 16-byte
+  // address: a broadcast) whose starts (NCH * e mod 8) fall in distinct bank groups for NCH = 9
+  // (prism geometry) and 10 (ConvDiff coefficients) -- no barrel shifter needed
+  __device__ __forceinline__ static void load_major_paired(uint32_t tile, int l, R (&out)[DS]) {
+    static_assert(CHUNKED && sizeof(R) == 8, "paired row loads: fp64 rows of whole 16-byte chunks");
+    static_assert((NCH * 1) % 8 != 0 && (NCH * 2) % 8 != 0 && (NCH * 3) % 8 != 0 && (NCH * 2) % 8 != NCH % 8 &&
+                  (NCH * 3) % 8 != NCH % 8 && (NCH * 3) % 8 != (NCH * 2) % 8,
+                  "4 rows per quarter-warp phase must start in distinct bank groups");
+    const uint32_t row = tile + static_cast<uint32_t>(l) * BYTES;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const uint4 v = lds128(row + 16u * c);
+      out[2 * c] = bits_to_real<double>(v.x, v.y);
+      out[2 * c + 1] = bits_to_real<double>(v.z, v.w);
+    }
+  }
+  __device__ __forceinline__ static void load_paired(uint32_t tile, int l, int w, R (&out)[DS]) {
+    if (w == 1) {
+      load_major_paired(tile, l, out);
+    } else {
+      load_interleaved(tile, l, w, out);
+    }
+  }
+
   // lane-interleaved output tile (datum d of element l at (l/W)*W*DS + d*W + l%W)
   __device__ __forceinline__ static void store_interleaved(uint32_t tile, int l, int w, const R (&in)[DS]) {
     const uint32_t base = tile + static_cast<uint32_t>((l / w) * w * DS + (l % w)) * sizeof(R);

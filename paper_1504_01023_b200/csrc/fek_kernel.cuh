@@ -274,10 +274,10 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
       int kind = 0, kind_point = -1;
       {
         R C[20], J2[3][3], J01[3][2], bound;
-        RowIO<R, 20>::load(pipe.coef(s), el, p.lane_width, C);
+        RowIO<R, 20>::load_paired(pipe.coef(s), el, p.lane_width, C);
         {
           R X[18];
-          RowIO<R, 18>::load(pipe.geo(s), el, p.lane_width, X);
+          RowIO<R, 18>::load_paired(pipe.geo(s), el, p.lane_width, X);
           prism_pair::level_geometry(X, z, bound, J2, J01);
         }
         // the previous tile's bulk stores have read the output tile by now (they left before
