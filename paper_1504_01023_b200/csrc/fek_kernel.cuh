@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
   // records each stage's tile in smem before arriving on the stage barrier, so
   // consumers read it after the wait; tiles past the end arrive without bytes.
   __shared__ long long s_tile[K::STAGES];
-  __shared__ unsigned s_out_done;  // PAIR: warps done writing the output tile (the last one stores it)
+  __shared__ unsigned s_out_done;  // warps done writing the output tile (the last one stores it)
   if (tid == 0) s_out_done = 0;
   long long static_next = blockIdx.x;
   auto issue_stage = [&](int s) {
@@ -250,7 +250,11 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
     // may still be in flight into this CTA's shared memory, so leaving would let
     // them land in a co-resident CTA's; the key is recorded, then the kernel traps.
     const bool stop = !landed || t >= pipe.tiles;
+    // The stage-release barrier is the tile's only CTA barrier.  Before it, every warp's lane 0
+    // waits until its own bulk stores of the previous tile have read the output tile (the last
+    // warp to finish a tile issues its store, below), so after it the output tile is free too.
     auto release = [&]() -> bool {
+      if ((tid & 31) == 0) bulk_wait_read<0>();
       if (__syncthreads_or(stop)) {
         if (!landed) {
           atomicMin(p.error_key, static_cast<unsigned long long>(KIND_PIPELINE_TIMEOUT));
@@ -280,13 +284,8 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
           RowIO<R, 18>::load_paired(pipe.geo(s), el, p.lane_width, X);
           prism_pair::level_geometry(X, z, bound, J2, J01);
         }
-        // the previous tile's bulk stores have read the output tile by now (they left before
-        // this tile's prologue): checked before the release barrier, which then also frees the
-        // output tile -- two CTA barriers per tile instead of three (C4 2.020 -> 2.004 ms).
-        // Per-warp output stores (no CTA barrier before them) measured slower: 2.028 ms.  The
-        // split-format store is issued by whichever warp finishes the tile last, so every warp's
-        // lane 0 waits on its own (possibly empty) bulk groups here.
-        if ((tid & 31) == 0) bulk_wait_read<0>();
+        // (release() also frees the output tile: C4 2.020 -> 2.004 ms for that merge; per-warp
+        // output stores measured slower, 2.028 ms)
         if (!release()) break;
         prism_pair::integrate_cd_level(J2, J01, C, bound, z, Ah, Bh, kind, kind_point);
       }
@@ -405,8 +404,19 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
       if (active) apply_rows<R, K::NS, K::NS>(p, e0 + tid, 0, A, B);
       continue;
     }
-    if (tid == 0) bulk_wait_read<0>();
-    __syncthreads();
+    // outputs: each warp writes its rows into the output tile, and the LAST warp to finish issues
+    // the tile's bulk store (shared-memory arrival counter) -- no CTA barrier, nobody waits for the
+    // slowest warp (the output tile was freed by the release barrier)
+    auto last_warp = [&]() -> bool {
+      fence_proxy_async_smem();
+      __syncwarp();
+      if ((tid & 31) != 0) return false;
+      __threadfence_block();
+      if (atomicAdd(&s_out_done, 1u) != K::THREADS / 32 - 1) return false;
+      __threadfence_block();
+      s_out_done = 0;  // the next tile's arrivals come after the next release barrier
+      return true;
+    };
     if (p.out_packed) {
       // packed rows [A row-major | b] (BatchResult.output_rows) laid out in
       // the output layout; pad lanes of a partial interleaved block get NaN
@@ -426,9 +436,7 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
           RowIO<R, DSO>::store_interleaved(out_a, tid, w, row);
         }
       }
-      fence_proxy_async_smem();
-      __syncthreads();
-      if (tid == 0) {
+      if (last_warp()) {
         const unsigned ob = padded * DSO * sizeof(R);
         char *go = static_cast<char *>(p.stiffness) + e0 * DSO * sizeof(R);
         const unsigned ob16 = ob & ~15u;
@@ -442,9 +450,7 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
       RowIO<R, K::NA>::store_major(out_a, tid, A);
       RowIO<R, K::NS>::store_major(out_b, tid, B);
     }
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (tid == 0) {
+    if (last_warp()) {
       const unsigned ab = count * K::NA * sizeof(R), bb = count * K::NS * sizeof(R);
       char *ga = static_cast<char *>(p.stiffness) + e0 * K::NA * sizeof(R);
       char *gb = static_cast<char *>(p.load) + e0 * K::NS * sizeof(R);
@@ -456,11 +462,8 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
       for (unsigned k = bb16; k < bb; k += 4) *reinterpret_cast<uint32_t *>(gb + k) = lds32(out_b + k);
     }
   }
-  if constexpr (K::PAIR) {
-    if ((tid & 31) == 0) bulk_wait_all<0>();  // the last-arriving warp's stores
-  }
+  if ((tid & 31) == 0) bulk_wait_all<0>();  // the last-arriving warps' stores: done reading smem at exit
   if (tid == 0) {
-    bulk_wait_all<0>();  // no bulk store may still be reading smem at exit
     if (p.scheduler) {
       // the last CTA out resets the queue for the next launch on this buffer
       __threadfence();
