@@ -695,8 +695,6 @@ def run_c5(args) -> int:
     torch.cuda.set_device(local)
     distributed = launched_by_torchrun()
     if distributed:
-        os.environ.setdefault("NCCL_DEBUG", "INFO")           # communicator lines on stderr
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     barrier = dist.barrier if distributed else None
     parts = [Part(*c) for c in c5_parts(world, rank)]
@@ -1040,6 +1038,9 @@ def _relaunch_under_torchrun(args, argv) -> int:
 
 def main(argv=None) -> int:
     args = parse(argv)
+    if launched_by_torchrun():
+        # NCCL communicator lines (ring/tree/NVLS setup) on stderr; set before torch loads NCCL
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
     if args.gpus > 1 and not launched_by_torchrun():
         return _relaunch_under_torchrun(args, argv)
     if args.impl == "reference":
