@@ -579,11 +579,13 @@ def _staging_buffer(device: int, nbytes: int) -> np.ndarray:
 
 
 def _copy_threads() -> int:
-    """Host copy threads of the staged pipeline: this rank's share of the host cores (<= 16)."""
+    """Host copy threads of the staged pipeline: this rank's share of the host cores, at most 8
+    (the cache-resident staging ring is copy-engine-bound beyond that: 452 ms per C5 step at 8
+    threads, 458 at 12, 464 at 6; tools/e2e_pageable.py)."""
     import os
 
     per_node = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
-    return max(1, min(16, (os.cpu_count() or 1) // per_node))
+    return max(1, min(8, (os.cpu_count() or 1) // per_node))
 
 
 def _aligned_f64(a) -> np.ndarray:
