@@ -124,3 +124,18 @@ def test_verify_batch_results_match_reference_corpus():
             res = integrate_batch(desc, batch)
             assert relative_difference(res.stiffness, g[f"A_{desc.short_name()}"]) <= 1e-12
             assert np.isfinite(res.load).all()
+
+
+def test_extended_tuner_sweeps_tiles_and_ctas(tmp_path):
+    """tune --launch: tile T x CTAs/SM rows in the reference's CSV schema plus two trailing columns."""
+    import csv
+
+    from paper_1504_01023_b200 import tune
+
+    out = tmp_path / "launch.csv"
+    assert tune.main(["--case", "C3", "--elements", "40000", "--repeats", "2", "--launch", "--out", str(out)]) == 0
+    rows = list(csv.DictReader(open(out)))
+    assert {int(r["tile_elements"]) for r in rows} == {64, 128, 256}
+    assert min(int(r["ctas_per_sm"]) for r in rows) == 1 and len(rows) >= 4
+    assert list(rows[0].keys())[-2:] == ["tile_elements", "ctas_per_sm"]
+    assert all(float(r["ns_per_element"]) > 0 for r in rows)
