@@ -1229,20 +1229,28 @@ __device__ __forceinline__ void integrate_cd_level(const R (&J2)[3][3], const R 
       for (int k = 0; k < 3; ++k) K[1 + k][1 + l] = rdet * fma(adj[k][0], M[0], fma(adj[k][1], M[1], adj[k][2] * M[2]));
     }
     const R L[3] = {R(lam(t, 0)), R(lam(t, 1)), R(lam(t, 2))};
+    // X_0 = (lam_0, -1, -1): its products need k1 + k2, formed once and shared (fused: one
+    // FMA instead of a product and two subtractions)
+    auto x0dot = [&](const R &k0, const R &k1, const R &k2) { return fma(L[0], k0, -(k1 + k2)); };
     static_for<3>([&](auto apc) {
       FEK_CI(ap, apc);
       R v[3];
 #pragma unroll
-      for (int al = 0; al < 3; ++al) v[al] = xdot<ap, true>(R(0), L[ap], K[al][0], K[al][1], K[al][2]);
+      for (int al = 0; al < 3; ++al)
+        v[al] = ap == 0 ? x0dot(K[al][0], K[al][1], K[al][2]) : xdot<ap, true>(R(0), L[ap], K[al][0], K[al][1], K[al][2]);
       static_for<3>([&](auto ac) {
         FEK_CI(a, ac);
-        SXX[a][ap] = xdot<a, F>(SXX[a][ap], L[a], v[0], v[1], v[2]);
+        if constexpr (F && a == 0) {
+          SXX[a][ap] = x0dot(v[0], v[1], v[2]);
+        } else {
+          SXX[a][ap] = xdot<a, F>(SXX[a][ap], L[a], v[0], v[1], v[2]);
+        }
       });
     });
     static_for<3>([&](auto ac) {
       FEK_CI(a, ac);
-      const R p = xdot<a, true>(R(0), L[a], K[0][3], K[1][3], K[2][3]);
-      const R q = xdot<a, true>(R(0), L[a], K[3][0], K[3][1], K[3][2]);
+      const R p = a == 0 ? x0dot(K[0][3], K[1][3], K[2][3]) : xdot<a, true>(R(0), L[a], K[0][3], K[1][3], K[2][3]);
+      const R q = a == 0 ? x0dot(K[3][0], K[3][1], K[3][2]) : xdot<a, true>(R(0), L[a], K[3][0], K[3][1], K[3][2]);
       static_for<3>([&](auto bc) {
         FEK_CI(ap, bc);
         mac<F>(SXY[a][ap], R(0.5 * lam(t, ap)), p);   // SXY / 2
@@ -1262,7 +1270,11 @@ __device__ __forceinline__ void integrate_cd_level(const R (&J2)[3][3], const R 
     for (int k = 0; k < 3; ++k) e[k] = fma(adj[k][0], wd[1], fma(adj[k][1], wd[2], adj[k][2] * wd[3]));
     static_for<3>([&](auto ac) {
       FEK_CI(a, ac);
-      SbX[a] = xdot<a, F>(SbX[a], L[a], e0, e[0], e[1]);
+      if constexpr (F && a == 0) {
+        SbX[a] = x0dot(e0, e[0], e[1]);
+      } else {
+        SbX[a] = xdot<a, F>(SbX[a], L[a], e0, e[0], e[1]);
+      }
       mac<F>(SbY[a], R(0.5 * lam(t, a)), e[2]);                        // SbY / 2
     });
   });
