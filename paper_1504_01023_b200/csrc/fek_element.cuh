@@ -1288,7 +1288,9 @@ __device__ __forceinline__ void integrate_cd_level(const R (&J2)[3][3], const R 
   // block b = z (l_b(z) = ell(z, z)) and the partner's b = 1 - z (ell(z, 1 - z)); with the
   // halves folded in, l'_b' terms are +-1 (compile-time signs) and l'_b = s (s = -1, +1 for b = 0, 1)
   static_assert(ell(0, 0) == ell(1, 1) && ell(0, 1) == ell(1, 0), "level factors swap between the levels");
-  const R sgn = z ? R(1) : R(-1);                                          // l'_own / (1/2)
+  // l'_own / (1/2) = -1, +1 for z = 0, 1: applied as a sign-bit flip on the ALU, not a DMUL
+  const unsigned long long sflip = z ? 0ull : 0x8000000000000000ull;
+  auto sgn_times = [&](R v) { return __longlong_as_double(static_cast<long long>(__double_as_longlong(v) ^ sflip)); };
   const R lcol[2] = {z ? R(ell(1, 0)) : R(ell(0, 0)), z ? R(ell(1, 1)) : R(ell(0, 1))};  // l_b'(z)
   constexpr double l_own = ell(0, 0), l_oth = ell(0, 1);
   R Po[18], Bo[3];  // the partner's row block: sent
@@ -1301,12 +1303,12 @@ __device__ __forceinline__ void integrate_cd_level(const R (&J2)[3][3], const R 
         FEK_CI(bp, b2c);
         const R u = bp ? fma(lcol[bp], SXX[a][ap], SXY[a][ap]) : fma(lcol[bp], SXX[a][ap], -SXY[a][ap]);
         const R v = bp ? fma(lcol[bp], SYX[a][ap], syy) : fma(lcol[bp], SYX[a][ap], -syy);
-        const R sv = sgn * v;
+        const R sv = sgn_times(v);
         Ah[6 * a + ap + 3 * bp] = fma(R(l_own), u, sv);
         Po[6 * a + ap + 3 * bp] = fma(R(l_oth), u, -sv);
       });
     });
-    const R sb = sgn * SbY[a];
+    const R sb = sgn_times(SbY[a]);
     Bh[a] = fma(R(l_own), SbX[a], sb);
     Bo[a] = fma(R(l_oth), SbX[a], -sb);
   });
