@@ -1,33 +1,39 @@
 // fek_kernel.cuh -- the persistent, TMA-pipelined integration kernel.
 //
 // One CTA = 128 threads (4 warps) = one tile of TILE = 128 elements at a
-// time, one element per thread.  CTAs are persistent (grid = SMs x resident
-// CTAs) and take tiles from a device queue (atomicAdd; static round-robin
-// t = blockIdx.x + i*gridDim.x without one).  Per tile i:
+// time, one element per thread -- except the fp64 prism ConvDiff kernel, which
+// runs each element on a lane pair (one zeta level per lane, fek_element.cuh
+// prism_pair) with 64-element tiles.  CTAs are persistent (grid = SMs x
+// resident CTAs) and take tiles from a device queue (atomicAdd; static
+// round-robin t = blockIdx.x + i*gridDim.x without one).  Per tile i:
 //
 //   1. the tile's geometry and coefficient byte ranges (contiguous in both
 //      the element-major and the lane-interleaved layout, because TILE is a
 //      multiple of every lane width) arrive by 1-D TMA bulk copies into stage
 //      i % STAGES; completion is counted on full[stage] (arrival + bytes);
 //   2. each thread pulls its element's rows into registers (conflict-free
-//      rotated 16-byte reads, fek_device.cuh); the QSS prism kernels read
-//      the coefficient row and form the 21 distinct Jacobian entries from
-//      the staged coordinates (their prologue);
-//   3. once every thread is done with the stage (CTA barrier), thread 0
-//      refills it with tile i + STAGES -- for the fp64 QSS prism kernels
-//      right after the prologue, so the refill overlaps the math;
+//      16-byte reads, fek_device.cuh); the QSS prism kernels read the
+//      coefficient row and form their distinct Jacobian entries from the
+//      staged coordinates (their prologue);
+//   3. once every thread is done with the stage -- the tile's ONLY CTA
+//      barrier -- thread 0 refills it with tile i + STAGES (for the fp64 QSS
+//      prism kernels right after the prologue, so the refill overlaps the
+//      math).  Before that barrier every warp's lane 0 has waited until its
+//      own bulk stores of tile i - 1 have read the output tile, so the
+//      barrier frees the output tile as well;
 //   4. the element math runs in registers (fek_element.cuh);
-//   5. A and b rows are written to one shared output tile (the exact global
-//      byte image) and leave the SM as two TMA bulk stores (full-line
-//      coalesced writes); the next tile waits until those stores have READ
-//      the tile (bulk_wait_read) before overwriting it.
+//   5. each warp writes its A and b rows into one shared output tile (the
+//      exact global byte image); the LAST warp to finish (shared-memory
+//      arrival counter) sends the tile out as two TMA bulk stores (full-line
+//      coalesced writes) -- nobody waits for the slowest warp.
 //
-// The barriers keep the four warps in step.  A warp-decoupled variant
-// (per-warp mbarrier release + per-warp output slices) was measured slower on
-// every case -- up to 12% on the FP64-bound prism kernel, whose unrolled SASS
-// thrashes the instruction cache once warps drift apart; per-warp output
-// stores alone gained nothing.  Geometry failures become one 64-bit key per element,
-// merged with atomicMin into the caller's error word.
+// A warp-decoupled variant (per-warp mbarrier release + per-warp output
+// slices) was measured slower on every case -- up to 12% on the FP64-bound
+// prism kernel, whose unrolled SASS thrashes the instruction cache once warps
+// drift apart; per-warp output stores alone lost too, and direct global stores
+// of the rows far more.  Geometry failures become one
+// 64-bit key per element, merged with atomicMin into the caller's error word.
+// With APPLY (fek_apply) step 5 is replaced by the matrix-free scatter.
 #pragma once
 
 #include "fek_element.cuh"
