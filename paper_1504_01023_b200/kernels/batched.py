@@ -542,17 +542,20 @@ def resolve_error_key(dd: _native.BatchDesc, err, stream: int) -> int:
 # host path: chunked H2D -> kernel -> D2H pipeline inside libfek
 # ---------------------------------------------------------------------------
 
-_stream_cache: dict[int, list] = {}
+_stream_cache: dict[tuple, list] = {}
 _stream_lock = threading.Lock()
 
 
 def _host_streams(device: int):
+    """The host pipeline's CUDA streams for this (device, host thread): concurrent integrate_batch
+    calls from several threads (the API is re-entrant, batched.py's contract) get their own."""
     import torch
 
+    key = (device, threading.get_ident())
     with _stream_lock:
-        if device not in _stream_cache:
-            _stream_cache[device] = [torch.cuda.Stream(device=device) for _ in range(HOST_STREAMS)]
-        return _stream_cache[device]
+        if key not in _stream_cache:
+            _stream_cache[key] = [torch.cuda.Stream(device=device) for _ in range(HOST_STREAMS)]
+        return _stream_cache[key]
 
 
 def host_chunk_elements(n: int) -> int:
@@ -561,7 +564,7 @@ def host_chunk_elements(n: int) -> int:
     return -(-chunk // 256) * 256
 
 
-_staging: dict[int, np.ndarray] = {}
+_staging: dict[tuple, np.ndarray] = {}
 
 
 def _needs_staging(*arrays) -> bool:
@@ -570,11 +573,13 @@ def _needs_staging(*arrays) -> bool:
 
 
 def _staging_buffer(device: int, nbytes: int) -> np.ndarray:
-    """Page-locked staging for fek_integrate_host_staged, kept per device and grown on demand."""
+    """Page-locked staging for fek_integrate_host_staged, kept per (device, host thread) and grown
+    on demand."""
+    key = (device, threading.get_ident())
     with _stream_lock:
-        buf = _staging.get(device)
+        buf = _staging.get(key)
         if buf is None or buf.nbytes < nbytes:
-            buf = _staging[device] = hostmem.empty(-(-nbytes // 8), pin=True)
+            buf = _staging[key] = hostmem.empty(-(-nbytes // 8), pin=True)
         return buf
 
 

@@ -45,6 +45,22 @@ def main():
 
     step(pinned)
     print(f"pinned: {min(step(pinned) for _ in range(args.reps)) * 1e3:.1f} ms", flush=True)
+    from concurrent.futures import ThreadPoolExecutor
+
+    descs = [KB.coerce_descriptor(c[1]) for c in bench.c5_parts(1, 0)]
+
+    def step_concurrent(batches):
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(len(batches)) as ex:
+            list(ex.map(lambda ib: integrate_batch(descs[ib[0]], ib[1]), enumerate(batches)))
+        return time.perf_counter() - t0
+
+    step_concurrent(pinned)
+    print(f"pinned, both batches concurrently (two host threads): "
+          f"{min(step_concurrent(pinned) for _ in range(args.reps)) * 1e3:.1f} ms", flush=True)
+    step_concurrent(plain)
+    print(f"pageable, both batches concurrently: {min(step_concurrent(plain) for _ in range(args.reps)) * 1e3:.1f} ms",
+          flush=True)
     orig = KB.host_chunk_elements
     for ch in [int(x) for x in args.chunks.split(",")]:
         KB.host_chunk_elements = (lambda n, ch=ch: ch) if ch else orig
