@@ -87,9 +87,11 @@ enum fek_status {
 #define FEK_KIND_PIPELINE_TIMEOUT 3 /* recorded just before the kernel traps (internal error) */
 /* The integration kernels classify on their own FMA-contracted det J against
  * 16 x the degeneracy tolerance; the reference rounds det J differently
- * (batched.py:151-163).  Beyond that bound both dets give the same class; within
- * it (never on a valid mesh) the kernel records NEAR at the element's first such
- * point and the caller re-derives the exact key with fek_classify. */
+ * (batched.py:151-163).  Beyond that bound both dets give the same class (fp64;
+ * fp32 rounding of det J is ~1e-6 diag^3, far above the tolerance, so the fp32
+ * kernels classify only approximately); within it (never on a valid mesh) the
+ * kernel records NEAR at the element's first such point and the caller re-derives
+ * the exact key with fek_classify. */
 #define FEK_KIND_NEAR 4
 
 typedef struct fek_batch_desc {
