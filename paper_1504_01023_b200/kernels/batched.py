@@ -559,8 +559,10 @@ def _host_streams(device: int):
 
 
 def host_chunk_elements(n: int) -> int:
-    """Pipeline chunk: ~8+ chunks for big batches, a multiple of 256 elements (every tile size)."""
-    chunk = max(16384, min(1 << 19, -(-n // 8)))
+    """Pipeline chunk: ~8+ chunks for big batches (at most 1 Mi elements: C5's 32M-element batches
+    ran 379 ms per step at 1 Mi vs 428 ms at 512 Ki on one box, tools/e2e_pageable.py), a
+    multiple of 256 elements (every tile size)."""
+    chunk = max(16384, min(1 << 20, -(-n // 8)))
     return -(-chunk // 256) * 256
 
 

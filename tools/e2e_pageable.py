@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--threads", default="4,8,12,16")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--chunks", default="0")
+    ap.add_argument("--streams", default="3")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -62,8 +63,17 @@ def main():
     print(f"pageable, both batches concurrently: {min(step_concurrent(plain) for _ in range(args.reps)) * 1e3:.1f} ms",
           flush=True)
     orig = KB.host_chunk_elements
+    orig_streams = KB.HOST_STREAMS
     for ch in [int(x) for x in args.chunks.split(",")]:
         KB.host_chunk_elements = (lambda n, ch=ch: ch) if ch else orig
+        for ns in [int(x) for x in args.streams.split(",")]:
+            KB.HOST_STREAMS = ns
+            KB._stream_cache.clear()
+            step(pinned)
+            print(f"pinned chunk={ch or 'default'} streams={ns}: {min(step(pinned) for _ in range(args.reps)) * 1e3:.1f} ms",
+                  flush=True)
+        KB.HOST_STREAMS = orig_streams
+        KB._stream_cache.clear()
         for t in [int(x) for x in args.threads.split(",")]:
             KB._copy_threads = lambda t=t: t
             step(plain)
