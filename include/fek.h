@@ -188,7 +188,9 @@ int fek_classify(const fek_batch_desc *d, void *cuda_stream);
 /* fek_integrate_host for PAGEABLE host buffers (plain malloc / numpy memory, as a reference
  * caller's ElementBatch holds them, layout.py:103-112): every pageable array among geometry /
  * coefficients / stiffness / load is staged through `host_staging` (page-locked, at least
- * fek_host_staging_bytes(d, n_streams, chunk_elements) bytes, 16-byte aligned) by
+ * fek_host_staging_bytes(d, n_streams, chunk_elements) bytes -- which looks at d's pointers:
+ * a 36 MiB cache-resident input ring when only inputs are pageable, chunk-sized slots when
+ * outputs are, 0 when nothing is -- 16-byte aligned) by
  * `copy_threads` host threads, chunk by chunk, so the host copies of chunk i overlap the DMA
  * and the kernels of chunks i-1, i-2; page-locked arrays are DMA'd directly.  Otherwise as
  * fek_integrate_host (same error semantics). */

@@ -563,6 +563,32 @@ StagePlan stage_plan(const fek_batch_desc *d, long long chunk) {
   return p;
 }
 
+// Pageable inputs go through a ring of 3 pieces of up to 12 MiB at the start of the staging
+// buffer (inside the host's last-level cache), each reused once the DMA after it completed.
+// Sweep on the GPU box (C5, tools/e2e_pageable.py; 385 ms page-locked): chunk-sized slots
+// 575 ms, rings of 4 MiB x 4 / 8 x 4 / 12 x 3 / 16 x 4 pieces 507 / 468 / 452 / 497 ms.
+struct StageRing {
+  int pieces = 0;
+  size_t piece_bytes = 0;
+};
+StageRing stage_ring(const StagePlan &tp) {
+  StageRing r;
+  r.pieces = 3;
+  r.piece_bytes = (tp.in / r.pieces) & ~static_cast<size_t>(255);
+  if (r.piece_bytes > (12u << 20)) r.piece_bytes = 12u << 20;
+  if (r.piece_bytes < (1u << 20)) r.pieces = 0;  // small batches: whole-slot staging
+  return r;
+}
+// page-locked staging bytes the pipeline needs for d's pageable arrays: the input ring alone when
+// only inputs are pageable, chunk-sized slots when outputs are (or the batch is too small for a
+// ring), nothing when every array is page-locked
+size_t staging_need(const fek_batch_desc *d, int n_streams, long long chunk, bool stage_in, bool stage_out) {
+  const StagePlan tp = stage_plan(d, chunk);
+  const StageRing ring = stage_ring(tp);
+  if (stage_out || (stage_in && ring.pieces == 0)) return static_cast<size_t>(n_streams) * tp.slot;
+  return stage_in ? ring.pieces * ring.piece_bytes : 0;
+}
+
 // The chunked H2D -> kernel -> D2H pipeline.  staging == nullptr: host buffers are DMA'd
 // directly (page-locked buffers overlap; pageable ones serialise in the driver).  Otherwise
 // every pageable array goes through the page-locked staging slots: the inputs of chunk i are
@@ -586,10 +612,10 @@ int host_pipeline(const fek_batch_desc *d, void *device_workspace, size_t worksp
   const bool packed = d->out_format == FEK_OUT_PACKED;
   if (!d->geometry || !d->coefficients || !d->stiffness || (!packed && !d->load)) return FEK_ERR_ARGUMENT;
   const StagePlan tp = stage_plan(d, chunk);
-  if (staging && (staging_bytes < static_cast<size_t>(n_streams) * tp.slot || !aligned16(staging)))
-    return FEK_ERR_WORKSPACE;
   const bool stage_in = staging && (pageable(d->geometry) || pageable(d->coefficients));
   const bool stage_out = staging && (pageable(d->stiffness) || (!packed && pageable(d->load)));
+  if (staging && (staging_bytes < staging_need(d, n_streams, chunk, stage_in, stage_out) || !aligned16(staging)))
+    return FEK_ERR_WORKSPACE;
 
   char *ws = static_cast<char *>(device_workspace);
   unsigned long long *dkey = reinterpret_cast<unsigned long long *>(ws);
@@ -613,14 +639,9 @@ int host_pipeline(const fek_batch_desc *d, void *device_workspace, size_t worksp
   std::vector<cudaEvent_t> slot_done(n_streams, nullptr);  // staged: the slot's last D2H finished
   std::vector<cudaEvent_t> in_free(n_streams, nullptr);    // staged: the slot's last H2D finished
   std::unique_ptr<CopyPool> pool;
-  // Pageable inputs go through a ring of 3 pieces of up to 12 MiB at the start of the staging
-  // buffer (inside the host's last-level cache), each reused once the DMA after it completed.
-  // Sweep on the GPU box (C5, tools/e2e_pageable.py; 385 ms page-locked): chunk-sized slots
-  // 575 ms, rings of 4 MiB x 4 / 8 x 4 / 12 x 3 / 16 x 4 pieces 507 / 468 / 452 / 497 ms.
-  int ring_pieces = 3;
-  size_t piece_bytes = (tp.in / ring_pieces) & ~static_cast<size_t>(255);
-  if (piece_bytes > (12u << 20)) piece_bytes = 12u << 20;
-  if (piece_bytes < (1u << 20)) ring_pieces = 0;  // small batches: whole-slot staging
+  const StageRing ring = stage_ring(tp);
+  const int ring_pieces = ring.pieces;
+  const size_t piece_bytes = ring.piece_bytes;
   std::vector<cudaEvent_t> ring_ev(ring_pieces, nullptr);
   std::vector<char> ring_used(ring_pieces, 0);
   unsigned long long ring_next = 0;
@@ -789,8 +810,10 @@ int fek_integrate_host(const fek_batch_desc *d, void *device_workspace, size_t w
 
 size_t fek_host_staging_bytes(const fek_batch_desc *d, int n_streams, int64_t chunk_elements) {
   if (!d || n_streams < 1 || chunk_elements < 1) return 0;
-  const long long chunk = round_chunk(chunk_elements);
-  return static_cast<size_t>(n_streams) * stage_plan(d, chunk).slot;
+  const bool packed = d->out_format == FEK_OUT_PACKED;
+  const bool stage_in = (d->geometry && pageable(d->geometry)) || (d->coefficients && pageable(d->coefficients));
+  const bool stage_out = (d->stiffness && pageable(d->stiffness)) || (!packed && d->load && pageable(d->load));
+  return staging_need(d, n_streams, round_chunk(chunk_elements), stage_in, stage_out);
 }
 
 int fek_integrate_host_staged(const fek_batch_desc *d, void *device_workspace, size_t workspace_bytes, int n_streams,
