@@ -153,7 +153,8 @@ int fek_integrate(const fek_batch_desc *d, void *cuda_stream);
  * arrays of d's real type; y and f accumulate with atomicAdd, so the summation order (and
  * the last bits of y, f) vary between runs.  QSS natural-path descriptors (geo_linear tets,
  * geo_generic prisms), element-major inputs; d->stiffness / d->load are unused; geometry
- * errors are reported in d->error_key exactly as by fek_integrate. */
+ * errors are reported in d->error_key exactly as by fek_integrate.  Node numbers must index
+ * x, y and f (unchecked here; apply_batch checks them). */
 int fek_apply(const fek_batch_desc *d, const int32_t *element_nodes, const void *x, void *y, void *f,
               void *cuda_stream);
 

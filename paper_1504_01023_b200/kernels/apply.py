@@ -56,6 +56,11 @@ def apply_batch(desc, batch: DeviceBatch, element_nodes, x, y=None, f=None, *, c
         if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == batch.dtype and t.dim() == 1
                 and t.is_contiguous() and t.device == dev):
             raise ValueError(f"{name} must be a contiguous 1-D CUDA tensor of the batch's dtype on {dev}")
+    if n:
+        lo, hi = torch.aminmax(element_nodes)
+        if int(lo) < 0 or int(hi) >= x.numel() or (y is not None and int(hi) >= y.numel()) or \
+                (f is not None and f is not False and int(hi) >= f.numel()):
+            raise ValueError(f"element_nodes must lie in [0, {x.numel()}) (got [{int(lo)}, {int(hi)}])")
     if y is None:
         y = torch.zeros_like(x)
     if f is None:

@@ -94,3 +94,14 @@ def test_apply_reports_geometry_errors_like_integrate_batch():
     with pytest.raises(fek.NativeLibraryError):
         fek.apply_batch(KernelDescriptor(Variant.SQS, fek.natural_path(et), pb, et), dev,
                         torch.from_numpy(nodes).cuda(), torch.from_numpy(x).cuda())
+
+
+def test_apply_rejects_out_of_range_nodes():
+    et, pb, spec = CASES[0]
+    geo, cof, nodes, x = _setup(et, pb, spec)
+    dev = DeviceBatch.from_host(ElementBatch.from_arrays(et, pb, geo, cof))
+    desc = KernelDescriptor(Variant.QSS, fek.natural_path(et), pb, et)
+    bad = nodes.copy()
+    bad[5, 2] = len(x)
+    with pytest.raises(ValueError):
+        fek.apply_batch(desc, dev, torch.from_numpy(bad).cuda(), torch.from_numpy(x).cuda())
