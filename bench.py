@@ -482,6 +482,22 @@ def measure_apply(key: str, steps: int, warmup: int):
 
     fused_ms = time_graph([Apply(True)], steps, warmup) / steps
     fused_y_ms = time_graph([Apply(False)], steps, warmup) / steps  # an iterative solver's A x (f assembled once)
+    # fused CSR assembly (pattern built once, untimed): values[csr(i, j)] += A_e, f += b_e
+    from paper_1504_01023_b200 import csr_pattern
+
+    row_ptr, col = csr_pattern(nodes, nn)
+    values = torch.zeros(col.numel(), dtype=torch.float64, device="cuda")
+
+    class Assemble:
+        stream = torch.cuda.current_stream().cuda_stream
+
+        def __call__(self):
+            _native.check(lib.fek_assemble(ctypes.byref(dd), nodes.data_ptr(), row_ptr.data_ptr(), col.data_ptr(),
+                                           values.data_ptr(), f.data_ptr(), self.stream), "fek_assemble")
+
+    assemble_ms = time_graph([Assemble()], steps, warmup) / steps
+    nnz = col.numel()
+    del row_ptr, col, values
     if int(err.item()) != -1:
         raise RuntimeError(f"{key} apply: geometry error key {int(err.item()) & 0xFFFFFFFFFFFFFFFF:#x}")
     L = Launcher(desc, geo, cof)
@@ -509,13 +525,16 @@ def measure_apply(key: str, steps: int, warmup: int):
     two_pass_floor_ms = integrate_ms + reread / (hbm * 1e9) * 1e3
     rec = {"workload": f"{cfg.text}: y += sum_e A_e x_e, f += sum_e b_e (matrix-free, fp64)", "elements": n,
            "nodes": nn, "descriptor": desc.short_name(), "fused_ms": fused_ms, "fused_value": n / (fused_ms / 1e3),
-           "unit": UNIT, "fused_y_only_ms": fused_y_ms, "integrate_store_ms": integrate_ms,
+           "unit": UNIT, "fused_y_only_ms": fused_y_ms, "assemble_csr_ms": assemble_ms, "csr_nnz": nnz,
+           "integrate_store_ms": integrate_ms,
            "two_pass_floor_ms": two_pass_floor_ms,
            "speedup_vs_two_pass_floor": two_pass_floor_ms / fused_ms, "two_pass_torch_ms": two_ms,
            "fused_stream_bytes_per_launch": fused_bytes,
            "note": "fused: element inputs + int32 connectivity streamed, A and b never stored; x gathers and "
-                   "y/f atomicAdds hit L2.  two_pass_floor = the integration launch storing A, b + re-reading "
-                   "them at the copy peak; two_pass_torch = that launch + torch gather / bmm / index_add"}
+                   "y/f atomicAdds hit L2.  assemble_csr: the same kernel scattering A_e into a CSR matrix "
+                   "(binary search per entry, atomicAdd).  two_pass_floor = the integration launch storing A, b "
+                   "+ re-reading them at the copy peak; two_pass_torch = that launch + torch gather / bmm / "
+                   "index_add"}
     del L, geo, cof, nodes
     torch.cuda.empty_cache()
     return rec

@@ -27,6 +27,8 @@
  *                          jacobian_at_point (JacobianData) of one element.
  *   fek_apply           <- (new) the element matrices consumed in
  *                          the kernel: matrix-free y += sum_e P_e^T A_e P_e x.
+ *   fek_assemble        <- (new) the same, assembled into a CSR
+ *                          global matrix and load vector.
  *   fek_checksum        <- (new) per-shard verification sums reduced with
  *                          NCCL across GPUs.
  *
@@ -157,6 +159,17 @@ int fek_integrate(const fek_batch_desc *d, void *cuda_stream);
  * x, y and f (unchecked here; apply_batch checks them). */
 int fek_apply(const fek_batch_desc *d, const int32_t *element_nodes, const void *x, void *y, void *f,
               void *cuda_stream);
+
+/* Global sparse assembly fused with the integration (the other consumer PAPER.md:121-123 names):
+ * for every element e of d,
+ *     values[k(node(e, r), node(e, s))] += A_e[r][s]      f[node(e, r)] += b_e[r]
+ * where k(i, j) is the position of column j in row i of the caller's CSR pattern (int32
+ * row_ptr[n_nodes + 1] and col[nnz], columns sorted within each row, containing every
+ * element's node pairs -- e.g. built by the Python csr_pattern).  A_e, b_e are fek_integrate's,
+ * kept in registers; values and f accumulate with atomicAdd (order, hence last bits, vary).
+ * Same descriptor rules as fek_apply; node numbers must be valid rows of the pattern. */
+int fek_assemble(const fek_batch_desc *d, const int32_t *element_nodes, const int32_t *row_ptr, const int32_t *col,
+                 void *values, void *f, void *cuda_stream);
 
 /* Launch geometry fek_integrate would use (for reporting / launch counting). */
 int fek_launch_config(const fek_batch_desc *d, int *grid, int *block, int *smem_bytes,

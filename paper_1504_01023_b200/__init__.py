@@ -9,8 +9,9 @@ hand-written sm_100a CUDA kernels in ``libfek.so`` (C-ABI: ``include/fek.h``).
 from .errors import (CounterMismatch, DegenerateElement, FeklabError, GeometryError, HeterogeneousBatch,
                      InvertedElement, NativeLibraryError, ShapeMismatch)
 from .geometry import DEGENERACY_REL_TOL, ElementGeometry, JacobianData
-from .kernels import (BatchResult, DeviceBatch, TrafficCounters, access_breakdown, apply_batch, global_accesses,
-                      integrate_batch, integrate_element, launch_config, phase_op_counts)
+from .kernels import (BatchResult, DeviceBatch, TrafficCounters, access_breakdown, apply_batch, assemble_batch,
+                      csr_pattern, global_accesses, integrate_batch, integrate_element, launch_config,
+                      phase_op_counts)
 from .layout import (ELEMENT_MAJOR, LANE_WIDTHS, BatchLayout, ElementBatch, LayoutKind, build_batch, convert,
                      extract, flat_length, pack_rows, read_batch, unpack_rows, write_batch)
 from .perfmodel import (B200_NOMINAL, BUILTIN_PROFILES, KernelCost, ProcessorProfile, b200_profile, efficiency,
@@ -24,7 +25,7 @@ __version__ = "0.1.0"
 __all__ = [
     "B200_NOMINAL", "BUILTIN_PROFILES", "KernelCost", "ProcessorProfile", "b200_profile", "efficiency",
     "kernel_cost", "limiting_intensity", "memory_requirements", "time_bound",
-    "BatchLayout", "BatchResult", "apply_batch", "CoefficientSet", "CounterMismatch", "DEGENERACY_REL_TOL", "DegenerateElement",
+    "BatchLayout", "BatchResult", "apply_batch", "assemble_batch", "csr_pattern", "CoefficientSet", "CounterMismatch", "DEGENERACY_REL_TOL", "DegenerateElement",
     "DeviceBatch", "ELEMENT_MAJOR", "ElementBatch", "ElementGeometry", "JacobianData", "ElementMatrix", "ElementType",
     "FeklabError", "GeometryError", "GeometryPath", "HeterogeneousBatch", "InvertedElement", "KernelDescriptor",
     "LANE_WIDTHS", "LayoutKind", "NativeLibraryError", "ProblemClass", "QuadratureRule", "ShapeFunctionTable",

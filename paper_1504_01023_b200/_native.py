@@ -82,6 +82,7 @@ SIGNATURES = {
                                         ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
     "fek_classify": (ctypes.c_int, [_DP, _P]),
     "fek_apply": (ctypes.c_int, [_DP, _P, _P, _P, _P, _P]),
+    "fek_assemble": (ctypes.c_int, [_DP, _P, _P, _P, _P, _P, _P]),
     "fek_error_detail": (ctypes.c_int, [_DP, ctypes.c_int64, ctypes.c_int32, _P, _P]),
     "fek_jacobian": (ctypes.c_int, [_DP, ctypes.c_int64, ctypes.c_int32, _P, _P]),
     "fek_checksum_scratch_bytes": (ctypes.c_size_t, []),

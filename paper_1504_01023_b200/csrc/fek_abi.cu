@@ -128,16 +128,19 @@ int validate(const fek_batch_desc *d, bool need_pointers) {
   return FEK_OK;
 }
 
-struct ApplyArgs {
+struct ApplyArgs {  // a consumer launch: fek_apply (mode 1) or fek_assemble (mode 2)
+  int mode;
   const int32_t *element_nodes;
   const void *x;
   void *y;
   void *f;
+  const int32_t *row_ptr;
+  const int32_t *col;
 };
 
 int launch(const fek_batch_desc *d, cudaStream_t stream, int *grid_out, int *block_out, int *smem_out,
            int *tile_out, bool do_launch, const ApplyArgs *ap = nullptr) {
-  const int idx = ap ? fek::apply_index(d->dtype, d->element, d->problem) : d->tile_elements
+  const int idx = ap ? fek::consumer_index(d->dtype, d->element, d->problem, ap->mode) : d->tile_elements
                       ? fek::tiled_index(d->dtype, d->element, d->problem,
                                          d->tile_elements == 64 ? 0 : (d->tile_elements == 128 ? 1 : 2))
                       : kernel_index(d->dtype, d->element, d->problem, d->variant, d->geometry_path);
@@ -170,6 +173,8 @@ int launch(const fek_batch_desc *d, cudaStream_t stream, int *grid_out, int *blo
   p.x = ap ? ap->x : nullptr;
   p.y = ap ? ap->y : nullptr;
   p.f = ap ? ap->f : nullptr;
+  p.row_ptr = ap ? ap->row_ptr : nullptr;
+  p.col = ap ? ap->col : nullptr;
   ke.fn<<<grid, ke.threads, ke.smem, stream>>>(p);
   FEK_CUDA(cudaGetLastError());
   return FEK_OK;
@@ -276,18 +281,29 @@ int fek_integrate(const fek_batch_desc *d, void *cuda_stream) {
   return launch(d, static_cast<cudaStream_t>(cuda_stream), nullptr, nullptr, nullptr, nullptr, true);
 }
 
-int fek_apply(const fek_batch_desc *d, const int32_t *element_nodes, const void *x, void *y, void *f,
-              void *cuda_stream) {
+static int consumer_launch(const fek_batch_desc *d, const ApplyArgs &ap, void *cuda_stream) {
   if (int rc = validate(d, false)) return rc;
   const bool natural = d->variant == FEK_QSS &&
                        d->geometry_path == (d->element == FEK_TETRAHEDRON ? FEK_GEO_LINEAR : FEK_GEO_GENERIC);
   if (!natural || d->layout != FEK_ELEMENT_MAJOR || d->tile_elements != 0) return FEK_ERR_ARGUMENT;
   if (d->n_elements == 0) return FEK_OK;
-  if (!d->geometry || !d->coefficients || !d->error_key || !element_nodes || !x || !y) return FEK_ERR_ARGUMENT;
+  if (!d->geometry || !d->coefficients || !d->error_key || !ap.element_nodes || !ap.y) return FEK_ERR_ARGUMENT;
+  if (ap.mode == fek::MODE_APPLY && !ap.x) return FEK_ERR_ARGUMENT;
+  if (ap.mode == fek::MODE_ASSEMBLE && (!ap.row_ptr || !ap.col)) return FEK_ERR_ARGUMENT;
   if (!aligned16(d->geometry) || !aligned16(d->coefficients) || reinterpret_cast<uintptr_t>(d->scheduler) % 8)
     return FEK_ERR_ALIGNMENT;
-  const ApplyArgs ap{element_nodes, x, y, f};
   return launch(d, static_cast<cudaStream_t>(cuda_stream), nullptr, nullptr, nullptr, nullptr, true, &ap);
+}
+
+int fek_apply(const fek_batch_desc *d, const int32_t *element_nodes, const void *x, void *y, void *f,
+              void *cuda_stream) {
+  return consumer_launch(d, ApplyArgs{fek::MODE_APPLY, element_nodes, x, y, f, nullptr, nullptr}, cuda_stream);
+}
+
+int fek_assemble(const fek_batch_desc *d, const int32_t *element_nodes, const int32_t *row_ptr, const int32_t *col,
+                 void *values, void *f, void *cuda_stream) {
+  return consumer_launch(d, ApplyArgs{fek::MODE_ASSEMBLE, element_nodes, nullptr, values, f, row_ptr, col},
+                         cuda_stream);
 }
 
 int fek_launch_config(const fek_batch_desc *d, int *grid, int *block, int *smem_bytes, int *tile_elements) {

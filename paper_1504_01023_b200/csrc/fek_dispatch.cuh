@@ -23,15 +23,18 @@ struct KernelEntry {
 constexpr int kBaseCount = 2 * 2 * 2 * 3 * 2;
 constexpr int kTiles[3] = {64, 128, 256};
 constexpr int kTiledCount = 2 * 2 * 2 * 3;
-constexpr int kIndexCount = kBaseCount + kTiledCount + 2 * 2 * 2;
+constexpr int kIndexCount = kBaseCount + kTiledCount + 2 * 2 * 2 * 2;
 inline int kernel_index(int dtype, int et, int pb, int var, int geo) {
   return (((dtype * 2 + et) * 2 + pb) * 3 + var) * 2 + geo;
 }
 inline int tiled_index(int dtype, int et, int pb, int tile_slot) {
   return kBaseCount + ((dtype * 2 + et) * 2 + pb) * 3 + tile_slot;
 }
-// the fused matrix-free apply (fek_apply) of the QSS natural-path kernels
-inline int apply_index(int dtype, int et, int pb) { return kBaseCount + kTiledCount + (dtype * 2 + et) * 2 + pb; }
+// the consumers of the QSS natural-path kernels: fused matrix-free apply (fek_apply, mode 1) and
+// CSR assembly (fek_assemble, mode 2)
+inline int consumer_index(int dtype, int et, int pb, int mode) {
+  return kBaseCount + kTiledCount + (((mode - 1) * 2 + dtype) * 2 + et) * 2 + pb;
+}
 
 void register_f64_tet_poisson(KernelEntry *table);
 void register_f64_tet_convdiff(KernelEntry *table);
@@ -71,7 +74,8 @@ void fill_case(KernelEntry *table, int dtype) {
   table[tiled_index(dtype, ET, PB, 0)] = entry<Traits<R, ET, PB, QSS, NAT, kTiles[0]>>();
   table[tiled_index(dtype, ET, PB, 1)] = entry<Traits<R, ET, PB, QSS, NAT, kTiles[1]>>();
   table[tiled_index(dtype, ET, PB, 2)] = entry<Traits<R, ET, PB, QSS, NAT, kTiles[2]>>();
-  table[apply_index(dtype, ET, PB)] = entry<Traits<R, ET, PB, QSS, NAT, 0, true>>();
+  table[consumer_index(dtype, ET, PB, MODE_APPLY)] = entry<Traits<R, ET, PB, QSS, NAT, 0, MODE_APPLY>>();
+  table[consumer_index(dtype, ET, PB, MODE_ASSEMBLE)] = entry<Traits<R, ET, PB, QSS, NAT, 0, MODE_ASSEMBLE>>();
 #endif
 }
 #endif

@@ -33,7 +33,8 @@
 // drift apart; per-warp output stores alone lost too, and direct global stores
 // of the rows far more.  Geometry failures become one
 // 64-bit key per element, merged with atomicMin into the caller's error word.
-// With APPLY (fek_apply) step 5 is replaced by the matrix-free scatter.
+// With a consumer MODE (fek_apply / fek_assemble) step 5 is replaced by the matrix-free scatter
+// or the CSR assembly scatter: A and b never leave the registers.
 #pragma once
 
 #include "fek_element.cuh"
@@ -52,12 +53,51 @@ struct LaunchParams {
   int out_packed;  // FEK_OUT_PACKED: rows [A | b] into `stiffness` in the output layout
   int out_width;   // output lane width (1 = element-major rows)
   unsigned long long *scheduler;  // [next tile, CTAs done] or null (static round-robin)
-  // fused matrix-free apply (Traits APPLY, fek_apply): y[node] += A_e x_e, f[node] += b_e
+  // consumers (Traits MODE): fek_apply  y[node] += A_e x_e,  fek_assemble  values[csr(i, j)] += A_e;
+  // both  f[node] += b_e
   const int *element_nodes;  // (n, NS) int32, element-major
-  const void *x;
-  void *y;
-  void *f;  // may be null
+  const void *x;             // apply: the vector
+  void *y;                   // apply: the result / assemble: the CSR values
+  void *f;                   // may be null
+  const int *row_ptr;        // assemble: CSR row pointers (n_nodes + 1)
+  const int *col;            // assemble: CSR column indices, sorted within each row
 };
+
+enum : int { MODE_STORE = 0, MODE_APPLY = 1, MODE_ASSEMBLE = 2 };
+
+// position of column j in CSR row i (the caller's pattern holds every element's node pairs)
+__device__ __forceinline__ int csr_find(const LaunchParams &p, int i, int j) {
+  int lo = __ldg(p.row_ptr + i), hi = __ldg(p.row_ptr + i + 1);
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(p.col + mid) <= j) {
+      lo = mid;
+    } else {
+      hi = mid;
+    }
+  }
+  return lo;
+}
+
+// values[csr(nodes[r], nodes[s])] += A[r][s] and f[nodes[r]] += b[r] for ROWS rows of one element
+// starting at R0 (A_rows: those rows, NS columns each): fp atomicAdd
+template <typename R, int NS, int ROWS>
+__device__ __forceinline__ void assemble_rows(const LaunchParams &p, long long e_local, int r0, const R *A_rows,
+                                              const R *B_rows) {
+  const int *nd = p.element_nodes + e_local * NS;
+  int node[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) node[s] = __ldg(nd + s);
+  R *values = static_cast<R *>(p.y);
+  R *f = static_cast<R *>(p.f);
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) {
+    const int i = node[r0 + r];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) atomicAdd(values + csr_find(p, i, node[s]), A_rows[NS * r + s]);
+    if (f) atomicAdd(f + i, B_rows[r]);
+  }
+}
 
 // y[nodes[r]] += sum_s A[r][s] x[nodes[s]] for rows r of one element (RB rows starting at R0 of
 // its A; A_rows holds those rows, NS columns each), f[nodes[r]] += B_rows[r]: fp atomicAdd
@@ -84,7 +124,7 @@ __device__ __forceinline__ void apply_rows(const LaunchParams &p, long long e_lo
 }
 
 // TILE_ = 0: the kernel's own tile; 64 / 128 / 256: the tuner's tile-size variants (fek_dispatch.cuh)
-template <typename R_, int ET_, int PB_, int VAR_, int GEO_, int TILE_ = 0, bool APPLY_ = false>
+template <typename R_, int ET_, int PB_, int VAR_, int GEO_, int TILE_ = 0, int MODE_ = MODE_STORE>
 struct Traits {
   using R = R_;
   static constexpr int ET = ET_, PB = PB_, VAR = VAR_, GEO = GEO_;
@@ -105,8 +145,9 @@ struct Traits {
                                VAR == QSS && sizeof(R) == 8;
   static constexpr int NATURAL_TILE = PAIR ? FEK_PAIR_TILE : 128;
   static constexpr int TILE = TILE_ ? TILE_ : NATURAL_TILE;  // elements per tile (a multiple of every lane width)
-  // fused matrix-free apply: A and b stay in registers, no output tile, no bulk stores
-  static constexpr bool APPLY = APPLY_;
+  // consumers (fused matrix-free apply, CSR assembly): A and b stay in registers, no output tile
+  static constexpr int MODE = MODE_;
+  static constexpr bool APPLY = MODE != MODE_STORE;
   static_assert(TILE % 64 == 0, "a tile must be a whole number of lane blocks for every lane width");
   static constexpr int LANES = PAIR ? 2 : 1;
   static constexpr int THREADS = TILE * LANES;
@@ -296,8 +337,11 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
         prism_pair::integrate_cd_level(J2, J01, C, bound, z, Ah, Bh, kind, kind_point);
       }
       if (act && z == 0 && kind) atomicMin(p.error_key, make_error_key(p.base + e0 + el, kind_point, kind));
-      if constexpr (K::APPLY) {
+      if constexpr (K::MODE == MODE_APPLY) {
         if (act) apply_rows<R, 6, 3>(p, e0 + el, 3 * z, Ah, Bh);  // lane z: rows a + 3z
+        continue;
+      } else if constexpr (K::MODE == MODE_ASSEMBLE) {
+        if (act) assemble_rows<R, 6, 3>(p, e0 + el, 3 * z, Ah, Bh);
         continue;
       }
       constexpr unsigned RB = sizeof(R);
@@ -406,8 +450,11 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) integrate_kernel(co
       if (!release()) break;
     }
     if (kind) atomicMin(p.error_key, make_error_key(e_abs, kind_point, kind));
-    if constexpr (K::APPLY) {
+    if constexpr (K::MODE == MODE_APPLY) {
       if (active) apply_rows<R, K::NS, K::NS>(p, e0 + tid, 0, A, B);
+      continue;
+    } else if constexpr (K::MODE == MODE_ASSEMBLE) {
+      if (active) assemble_rows<R, K::NS, K::NS>(p, e0 + tid, 0, A, B);
       continue;
     }
     // outputs: each warp writes its rows into the output tile, and the LAST warp to finish issues

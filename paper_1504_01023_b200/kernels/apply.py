@@ -1,6 +1,8 @@
-"""Matrix-free operator application fused with the integration.
+"""Consumers of the element matrices fused with the integration.
 
     y, f = apply_batch(desc, device_batch, element_nodes, x)      # y += A x, f += b (assembled)
+    row_ptr, col = csr_pattern(element_nodes, n_nodes)            # the global matrix's sparsity
+    values, f = assemble_batch(desc, device_batch, element_nodes, row_ptr, col)   # CSR A, f
 
 The paper stops at the element matrices and leaves their use open: assembly, or "without
 assembly, in the so called matrix-free approaches", the output possibly kept
@@ -12,7 +14,8 @@ kernel's A_e and b_e stay in registers and are consumed in place,
 
 so a Krylov solver's operator application costs one pass over the element inputs (plus the
 connectivity and the gathered x) instead of integrate -> store 36 + 6 reals per element ->
-read them back.  The sums use atomicAdd, so the order in which element contributions land --
+read them back.  ``fek_assemble`` is the other consumer the paper names, assembly: the same
+registers scattered into a CSR global matrix (``values[csr(i, j)] += A_e[r][s]``).  The sums use atomicAdd, so the order in which element contributions land --
 and the last bits of y and f -- vary between runs; A_e and b_e themselves are bitwise the ones
 ``integrate_batch`` returns.  There is no CPU path.
 """
@@ -84,3 +87,79 @@ def apply_batch(desc, batch: DeviceBatch, element_nodes, x, y=None, f=None, *, c
             if key != _native.NO_ERROR:
                 _raise_geometry(key, lambda e, q: _device_error_detail(dd, e - base_index, q, stream))
     return y, (None if f is False else f)
+
+
+def csr_pattern(element_nodes, n_nodes: int):
+    """(row_ptr, col) int32 CUDA tensors: the CSR sparsity of sum_e P_e^T A_e P_e -- every node
+    pair that shares an element, columns sorted within each row (built on the device)."""
+    import torch
+
+    nodes = element_nodes.long()
+    n, ns = nodes.shape
+    keys = (nodes[:, :, None] * n_nodes + nodes[:, None, :]).reshape(-1)
+    keys = torch.unique(keys)  # sorted
+    rows = keys // n_nodes
+    col = (keys - rows * n_nodes).to(torch.int32)
+    row_ptr = torch.zeros(n_nodes + 1, dtype=torch.int64, device=nodes.device)
+    row_ptr[1:] = torch.cumsum(torch.bincount(rows, minlength=n_nodes), 0)
+    if int(row_ptr[-1]) >= 2 ** 31:
+        raise ValueError("pattern too large for int32 CSR")
+    return row_ptr.to(torch.int32), col
+
+
+def assemble_batch(desc, batch: DeviceBatch, element_nodes, row_ptr, col, values=None, f=None, *,
+                   check: bool = True, base_index: int = 0):
+    """values += CSR(sum_e P_e^T A_e P_e) and f += sum_e P_e^T b_e for a device batch.
+
+    ``row_ptr`` / ``col``: the CSR pattern (``csr_pattern``); ``values``: its nnz accumulators
+    (zeros when None); ``f``: node-indexed load accumulator (zeros of n_nodes when None, False to
+    skip).  Same descriptor / batch rules and errors as ``apply_batch``.  Returns (values, f).
+    """
+    import torch
+
+    desc = coerce_descriptor(desc)
+    _check_match(desc, batch)
+    if not isinstance(batch, DeviceBatch):
+        raise TypeError("assemble_batch takes a DeviceBatch (inputs in HBM)")
+    if batch.layout != ELEMENT_MAJOR:
+        raise ValueError("assemble_batch needs an element-major batch (DeviceBatch.convert(ELEMENT_MAJOR))")
+    n, ns = batch.n_elements, desc.element.n_shape
+    dev = batch.geometry_data.device
+    for name, t, dt in (("element_nodes", element_nodes, torch.int32), ("row_ptr", row_ptr, torch.int32),
+                        ("col", col, torch.int32)):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == dt and t.is_contiguous() and t.device == dev):
+            raise ValueError(f"{name} must be a contiguous int32 CUDA tensor on {dev}")
+    if tuple(element_nodes.shape) != (n, ns):
+        raise ValueError(f"element_nodes must have shape ({n}, {ns})")
+    n_nodes, nnz = row_ptr.numel() - 1, col.numel()
+    if n:
+        lo, hi = torch.aminmax(element_nodes)
+        if int(lo) < 0 or int(hi) >= n_nodes:
+            raise ValueError(f"element_nodes must lie in [0, {n_nodes}) (got [{int(lo)}, {int(hi)}])")
+    if values is None:
+        values = torch.zeros(nnz, dtype=batch.dtype, device=dev)
+    if f is None:
+        f = torch.zeros(n_nodes, dtype=batch.dtype, device=dev)
+    for name, t, size in (("values", values, nnz),) + (() if f is False else (("f", f, n_nodes),)):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == batch.dtype and t.dim() == 1
+                and t.numel() == size and t.is_contiguous() and t.device == dev):
+            raise ValueError(f"{name} must be a contiguous 1-D CUDA tensor of {size} {batch.dtype} on {dev}")
+    lib = _native.load()
+    dtype_code = _native.DTYPE["float64" if batch.dtype == torch.float64 else "float32"]
+    err = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    dd = _desc_struct(desc, ELEMENT_MAJOR, n, base_index, dtype_code, batch.geometry_data.data_ptr(),
+                      batch.coefficient_data.data_ptr(), 0, 0, err.data_ptr())
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream().cuda_stream
+        dd.scheduler = _tile_queue(dev, stream).data_ptr()
+        rc = lib.fek_assemble(ctypes.byref(dd), element_nodes.data_ptr(), row_ptr.data_ptr(), col.data_ptr(),
+                              values.data_ptr(), None if f is False else f.data_ptr(), stream)
+        if rc == _native.ERR_ARGUMENT:
+            raise NativeLibraryError(f"fek_assemble: {desc.short_name()} is not a QSS natural-path descriptor "
+                                     "or the batch is not element-major")
+        _native.check(rc, "fek_assemble")
+        if check:
+            key = resolve_error_key(dd, err, stream)
+            if key != _native.NO_ERROR:
+                _raise_geometry(key, lambda e, q: _device_error_detail(dd, e - base_index, q, stream))
+    return values, (None if f is False else f)

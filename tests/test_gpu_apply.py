@@ -105,3 +105,39 @@ def test_apply_rejects_out_of_range_nodes():
     bad[5, 2] = len(x)
     with pytest.raises(ValueError):
         fek.apply_batch(desc, dev, torch.from_numpy(bad).cuda(), torch.from_numpy(x).cuda())
+
+
+@pytest.mark.parametrize("et,pb,spec", CASES, ids=lambda c: getattr(c, "value", None) or str(getattr(c, "nx", c)))
+def test_assemble_matches_oracle(et, pb, spec):
+    """CSR assembly fused with the integration: every stored entry within 1e-13 of the sum of its
+    contributions' magnitudes against the oracle's matrices summed per node pair on the host."""
+    geo, cof, nodes, x = _setup(et, pb, spec)
+    desc = KernelDescriptor(Variant.QSS, fek.natural_path(et), pb, et)
+    A, b = O.integrate("qss", desc.geometry_path.value, pb.value, et.value, geo, cof)
+    nn = len(x)
+    dev = DeviceBatch.from_host(ElementBatch.from_arrays(et, pb, geo, cof))
+    tn = torch.from_numpy(nodes).cuda()
+    row_ptr, col = fek.csr_pattern(tn, nn)
+    values, f = fek.assemble_batch(desc, dev, tn, row_ptr, col)
+    rp, cl = row_ptr.cpu().numpy(), col.cpu().numpy()
+    assert (np.diff(rp) > 0).all() and all((np.diff(cl[rp[i]:rp[i + 1]]) > 0).all() for i in range(0, nn, 97))
+    rows = np.repeat(np.arange(nn), np.diff(rp))
+    keys = rows.astype(np.int64) * nn + cl
+    pr = np.repeat(nodes[:, :, None], nodes.shape[1], 2).reshape(-1).astype(np.int64)
+    pc = np.repeat(nodes[:, None, :], nodes.shape[1], 1).reshape(-1).astype(np.int64)
+    pos = np.searchsorted(keys, pr * nn + pc)
+    ref, mag = np.zeros(len(cl)), np.zeros(len(cl))
+    np.add.at(ref, pos, A.reshape(-1))
+    # scale: each contribution's element-matrix magnitude (entries that vanish exactly in the
+    # reference's arithmetic come out at rounding level in the kernel's)
+    np.add.at(mag, pos, np.repeat(np.abs(A).reshape(len(A), -1).max(1), A.shape[1] * A.shape[2]))
+    got = values.cpu().numpy()
+    assert (np.abs(got - ref) <= 1e-13 * mag + 1e-300).all()
+    y_ref, f_ref, _, fm = _scatter(A, b, nodes, x, nn)
+    assert (np.abs(f.cpu().numpy() - f_ref) <= 1e-13 * fm + 1e-300).all()
+    # the assembled matrix applied to x equals the fused apply
+    y, _ = fek.apply_batch(desc, dev, tn, torch.from_numpy(x).cuda(), f=False)
+    csr = torch.sparse_csr_tensor(row_ptr.long(), col.long(), values, size=(nn, nn))
+    y2 = (csr @ torch.from_numpy(x).cuda().unsqueeze(1)).squeeze(1)
+    _, _, ym, _ = _scatter(A, b, nodes, x, nn)
+    assert bool(((y - y2).abs().cpu() <= torch.from_numpy(2e-13 * ym + 1e-300)).all())
