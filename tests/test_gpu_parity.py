@@ -255,7 +255,7 @@ def test_fp32_variants_within_stated_tolerance():
             assert rel(b, z["b_algorithm1"]).max() < 1e-4, desc.short_name()
 
 
-@pytest.mark.parametrize("n", [0, 1, 2, 127, 128, 129, 255, 1000, 40000])
+@pytest.mark.parametrize("n", [0, 1, 2, 63, 64, 65, 127, 128, 129, 255, 1000, 40000])
 def test_ragged_sizes_and_chunking(n):
     rng = np.random.default_rng(n)
     from oracle.numpy_oracle import integrate as oracle
@@ -268,6 +268,9 @@ def test_ragged_sizes_and_chunking(n):
         desc = case_descriptors(et, pb)[0]
         res = integrate_batch(desc, batch)
         assert res.stiffness.shape == (n, et.n_shape, et.n_shape)
+        dres = integrate_batch(desc, DeviceBatch.from_host(batch))  # device path: tile tails (64 / 128)
+        assert np.array_equal(dres.stiffness.cpu().numpy(), res.stiffness)
+        assert np.array_equal(dres.load.cpu().numpy(), res.load)
         if n:
             A, b = oracle(desc.variant.value, desc.geometry_path.value, pb.value, et.value, geo, cof)
             assert rel(res.stiffness, A).max() <= TOL
