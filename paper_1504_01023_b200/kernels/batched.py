@@ -105,6 +105,21 @@ class BatchResult:
         self.stiffness = rows[:, : ns * ns].reshape(n, ns, ns)
         self.load = rows[:, ns * ns:]
 
+    def check_errors(self) -> None:
+        """For a device result made with ``check=False`` (e.g. inside a CUDA graph): read the
+        error word (synchronises), resolve a NEAR key with the exact pass, and raise the
+        reference's exception if an element is degenerate or inverted."""
+        launch = getattr(self, "_launch", None)
+        if launch is None:
+            return
+        import torch
+
+        dd, _, base_index = launch
+        stream = torch.cuda.current_stream().cuda_stream  # where the caller ran / replayed the launch
+        key = resolve_error_key(dd, self.error_word, stream)
+        if key != _native.NO_ERROR:
+            _raise_geometry(key, lambda e, q: _device_error_detail(dd, e - base_index, q, stream))
+
     def element_matrix(self, e: int) -> ElementMatrix:
         if not 0 <= e < self.n_elements:
             raise IndexError(f"element index {e} out of range")
@@ -508,6 +523,7 @@ def _integrate_device(desc: KernelDescriptor, batch: DeviceBatch, out_layout, ch
         result = BatchResult(desc, n, A, b, _traffic(desc, n), olayout, flat)
         result.error_word = err
         result._queue = queue
+        result._launch = (dd, stream, base_index)
         if check:
             key = resolve_error_key(dd, err, stream)
             if key != _native.NO_ERROR:

@@ -10,6 +10,7 @@ fill) must work on every replay.
 import numpy as np
 import pytest
 
+import paper_1504_01023_b200 as fek
 from conftest import golden
 from paper_1504_01023_b200 import (DeviceBatch, ElementBatch, ElementType, ProblemClass, case_descriptors,
                                    integrate_batch)
@@ -48,6 +49,15 @@ def test_capture_and_replay(et, pb):
         want = integrate_batch(desc, DeviceBatch.from_host(ElementBatch.from_arrays(et, pb, g_k, c_k)))
         assert torch.equal(res.stiffness, want.stiffness) and torch.equal(res.load, want.load)
         assert int(res.error_word.item()) == -1
+        res.check_errors()  # no error: returns
+    # an inverted element in the captured buffers: the replay's error word, resolved and raised
+    bad = geo.copy()
+    bad[7] = -bad[7]
+    db.geometry_data.copy_(torch.from_numpy(bad.reshape(-1)))
+    graph.replay()
+    with pytest.raises(fek.InvertedElement) as err:
+        res.check_errors()
+    assert err.value.element_index == 7
 
 
 def test_bench_graph_timing_does_every_step():
