@@ -416,3 +416,27 @@ def test_out_arrays_are_validated_before_the_launch():
         integrate_batch(desc, dev, out=ok, packed=True)
     with pytest.raises(TypeError):
         integrate_batch(desc, host, out=ok)
+
+
+def test_concurrent_host_calls_from_two_threads():
+    """integrate_batch is re-entrant (batched.py's contract): two host threads integrating different
+    host batches at once (own streams and staging per thread) get the sequential results bitwise."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_1504_01023_b200 import mesh
+
+    jobs = []
+    for et, pb, k in ((TET, CONVDIFF, 1), (PRISM, CONVDIFF, 2), (PRISM, POISSON, 3)):
+        spec = mesh.spec_for_element_count(et, 600_000)
+        geo = mesh.geometry_rows(spec)
+        cof = mesh.coefficient_rows(spec.n_elements, pb, et, k)
+        batch = ElementBatch.from_arrays(et, pb, geo, cof)
+        plain = ElementBatch(et, pb, batch.n_elements, batch.layout, np.array(batch.geometry_data),
+                             np.array(batch.coefficient_data))  # pageable: the staged path
+        desc = KernelDescriptor(Variant.QSS, fek.natural_path(et), pb, et)
+        jobs += [(desc, batch), (desc, plain)]
+    want = [integrate_batch(d, b) for d, b in jobs]
+    with ThreadPoolExecutor(3) as ex:
+        got = list(ex.map(lambda j: integrate_batch(*j), jobs))
+    for w, g in zip(want, got):
+        assert np.array_equal(w.stiffness, g.stiffness) and np.array_equal(w.load, g.load)
