@@ -198,3 +198,35 @@ def test_config_window_is_the_prefix_of_the_full_configuration():
         g, c = mesh.config_rows(cfg)
         gw, cw = mesh.config_window(cfg, 50_001)
         assert np.array_equal(g[:50_001], gw) and np.array_equal(c[:50_001], cw)
+
+
+def test_bind_exception_types_makes_the_boundary_raise_host_classes():
+    """errors.bind_exception_types(feklab.errors): the drop-in raises the host package's classes
+    (looked up at raise time by kernels/batched.py, kernels/scalar.py and geometry.py)."""
+    import types
+
+    from paper_1504_01023_b200 import errors
+    from paper_1504_01023_b200.kernels import batched
+
+    saved = {n: getattr(errors, n) for n in errors.BOUNDARY_TYPES}
+
+    class HostGeometryError(Exception):
+        def __init__(self, message, element_index=None, point_index=None):
+            super().__init__(message)
+            self.element_index, self.point_index = element_index, point_index
+
+    host = types.SimpleNamespace(GeometryError=HostGeometryError,
+                                 DegenerateElement=type("DegenerateElement", (HostGeometryError,), {}),
+                                 InvertedElement=type("InvertedElement", (HostGeometryError,), {}),
+                                 ShapeMismatch=type("ShapeMismatch", (Exception,), {}))
+    try:
+        errors.bind_exception_types(host)
+        with pytest.raises(host.InvertedElement) as err:
+            batched._raise_geometry((17, 3, 2), lambda e, q: (-0.5, 1e-14))
+        assert (err.value.element_index, err.value.point_index) == (17, 3)
+        assert "det J = -5.000e-01 < 0" in str(err.value)
+    finally:
+        for n, cls in saved.items():
+            setattr(errors, n, cls)
+    with pytest.raises(fek.InvertedElement):
+        batched._raise_geometry((17, 3, 2), lambda e, q: (-0.5, 1e-14))
