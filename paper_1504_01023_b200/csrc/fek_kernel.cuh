@@ -177,9 +177,15 @@ struct Traits {
       ((PRISM_P || (LAZY_X && PB == CONV_DIFF)) ? 1 : ((ET == TET && PB == POISSON) ? 3 : 2));
   static constexpr int MIN_BLOCKS_ = (F32_PRISM_CD || PRISM_P || (ET == TET && PB == POISSON)) ? 3 : 2;
   // (PAIR: 2 CTAs x 256 threads = 16 warps/SM at <= 128 registers)
-  static constexpr int STAGES = P32 ? 2 : STAGES_;
+#ifndef FEK_PAIR_STAGES
+#define FEK_PAIR_STAGES 1
+#endif
+#ifndef FEK_PAIR_CTAS
+#define FEK_PAIR_CTAS 4
+#endif
+  static constexpr int STAGES = P32 ? 2 : (PAIR ? FEK_PAIR_STAGES : STAGES_);
   // resident CTAs scale with the tile so the register budget per thread stays the natural one
-  static constexpr int MIN_BLOCKS_N = P32 ? 4 : (PAIR ? 256 / NATURAL_TILE : MIN_BLOCKS_);
+  static constexpr int MIN_BLOCKS_N = P32 ? 4 : (PAIR ? FEK_PAIR_CTAS * 64 / NATURAL_TILE : MIN_BLOCKS_);
   static constexpr int MIN_BLOCKS = (MIN_BLOCKS_N * NATURAL_TILE / TILE) > 0 ? (MIN_BLOCKS_N * NATURAL_TILE / TILE) : 1;
   static constexpr unsigned GEO_TILE_BYTES = TILE * DSG * sizeof(R);
   static constexpr unsigned COEF_TILE_BYTES = TILE * DSC * sizeof(R);
