@@ -95,6 +95,9 @@ enum fek_status {
  * kernel records NEAR at the element's first such point and the caller re-derives
  * the exact key with fek_classify. */
 #define FEK_KIND_NEAR 4
+/* fek_assemble: the CSR pattern has no entry for a node pair of the element (no point: the
+ * smallest such element wins); that contribution is skipped, nothing is written out of place */
+#define FEK_KIND_PATTERN 5
 
 typedef struct fek_batch_desc {
   int32_t element;        /* enum fek_element                                   */
@@ -167,7 +170,8 @@ int fek_apply(const fek_batch_desc *d, const int32_t *element_nodes, const void 
  * row_ptr[n_nodes + 1] and col[nnz], columns sorted within each row, containing every
  * element's node pairs -- e.g. built by the Python csr_pattern).  A_e, b_e are fek_integrate's,
  * kept in registers; values and f accumulate with atomicAdd (order, hence last bits, vary).
- * Same descriptor rules as fek_apply; node numbers must be valid rows of the pattern. */
+ * Same descriptor rules as fek_apply; node numbers must be valid rows of the pattern, and a
+ * node pair missing from it is recorded in d->error_key as FEK_KIND_PATTERN. */
 int fek_assemble(const fek_batch_desc *d, const int32_t *element_nodes, const int32_t *row_ptr, const int32_t *col,
                  void *values, void *f, void *cuda_stream);
 

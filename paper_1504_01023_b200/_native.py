@@ -23,7 +23,7 @@ ABI_VERSION = 4
 NO_ERROR = 0xFFFFFFFFFFFFFFFF
 
 OK, ERR_ARGUMENT, ERR_ALIGNMENT, ERR_CUDA, ERR_WORKSPACE, ERR_GEOMETRY = range(6)
-KIND_DEGENERATE, KIND_INVERTED, KIND_PIPELINE_TIMEOUT, KIND_NEAR = 1, 2, 3, 4
+KIND_DEGENERATE, KIND_INVERTED, KIND_PIPELINE_TIMEOUT, KIND_NEAR, KIND_PATTERN = 1, 2, 3, 4, 5
 
 # enum codes (fek.h)
 ELEMENT = {"tet": 0, "prism": 1}

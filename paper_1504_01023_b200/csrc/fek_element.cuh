@@ -45,6 +45,8 @@ constexpr int KIND_PIPELINE_TIMEOUT = 3;
 // |det J| within NEAR_TOL_FACTOR * tol at the element's first flagged point: the kernels' FMA det
 // cannot decide the class the reference's way there; fek_classify re-derives the key exactly
 constexpr int KIND_NEAR = 4;
+// fek_assemble: an element's node pair (row r, any column) is not in the caller's CSR pattern
+constexpr int KIND_PATTERN = 5;
 constexpr int ERROR_BLOCK_SHIFT = 13;  // batched.py:50 BLOCK_ELEMENTS = 8192
 
 // Error key ordering = the reference's first-error rule (batched.py:528-533,

@@ -68,6 +68,7 @@ enum : int { MODE_STORE = 0, MODE_APPLY = 1, MODE_ASSEMBLE = 2 };
 // position of column j in CSR row i (the caller's pattern holds every element's node pairs)
 __device__ __forceinline__ int csr_find(const LaunchParams &p, int i, int j) {
   int lo = __ldg(p.row_ptr + i), hi = __ldg(p.row_ptr + i + 1);
+  if (hi <= lo) return -1;  // empty row
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
     if (__ldg(p.col + mid) <= j) {
@@ -76,7 +77,7 @@ __device__ __forceinline__ int csr_find(const LaunchParams &p, int i, int j) {
       hi = mid;
     }
   }
-  return lo;
+  return __ldg(p.col + lo) == j ? lo : -1;  // -1: (i, j) is not in the pattern
 }
 
 // values[csr(nodes[r], nodes[s])] += A[r][s] and f[nodes[r]] += b[r] for ROWS rows of one element
@@ -94,7 +95,14 @@ __device__ __forceinline__ void assemble_rows(const LaunchParams &p, long long e
   for (int r = 0; r < ROWS; ++r) {
     const int i = node[r0 + r];
 #pragma unroll
-    for (int s = 0; s < NS; ++s) atomicAdd(values + csr_find(p, i, node[s]), A_rows[NS * r + s]);
+    for (int s = 0; s < NS; ++s) {
+      const int k = csr_find(p, i, node[s]);
+      if (k >= 0) {
+        atomicAdd(values + k, A_rows[NS * r + s]);
+      } else {  // a pattern that misses this element's pair: reported, never written elsewhere
+        atomicMin(p.error_key, make_error_key(p.base + e_local, -1, KIND_PATTERN));  // by element alone
+      }
+    }
     if (f) atomicAdd(f + i, B_rows[r]);
   }
 }

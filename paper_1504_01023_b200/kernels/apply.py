@@ -132,6 +132,15 @@ def assemble_batch(desc, batch: DeviceBatch, element_nodes, row_ptr, col, values
     if tuple(element_nodes.shape) != (n, ns):
         raise ValueError(f"element_nodes must have shape ({n}, {ns})")
     n_nodes, nnz = row_ptr.numel() - 1, col.numel()
+    if n_nodes < 0 or row_ptr.dim() != 1 or col.dim() != 1:
+        raise ValueError("row_ptr and col must be 1-D (row_ptr has n_nodes + 1 entries)")
+    # a well-formed CSR structure (the kernel searches it; pairs it lacks are reported below)
+    if int(row_ptr[0]) != 0 or int(row_ptr[-1]) != nnz or (n_nodes and bool((row_ptr[1:] < row_ptr[:-1]).any())):
+        raise ValueError(f"row_ptr must rise from 0 to nnz = {nnz}")
+    if nnz:
+        clo, chi = torch.aminmax(col)
+        if int(clo) < 0 or int(chi) >= n_nodes:
+            raise ValueError(f"col must lie in [0, {n_nodes}) (got [{int(clo)}, {int(chi)}])")
     if n:
         lo, hi = torch.aminmax(element_nodes)
         if int(lo) < 0 or int(hi) >= n_nodes:
@@ -159,7 +168,36 @@ def assemble_batch(desc, batch: DeviceBatch, element_nodes, row_ptr, col, values
                                      "or the batch is not element-major")
         _native.check(rc, "fek_assemble")
         if check:
+            raw = int(err.item()) & _native.NO_ERROR
             key = resolve_error_key(dd, err, stream)
+            if key == _native.NO_ERROR and raw != _native.NO_ERROR:
+                # an earlier NEAR key (resolved: no geometry error) may have hidden a pattern miss
+                miss = _first_pattern_miss(element_nodes, row_ptr, col)
+                key = _native.NO_ERROR if miss is None else (base_index + miss, None, _native.KIND_PATTERN)
             if key != _native.NO_ERROR:
+                element, _, kind = _native.decode_error(key) if isinstance(key, int) else key
+                if kind == _native.KIND_PATTERN:
+                    raise ValueError(f"the CSR pattern has no entry for a node pair of element {element}; "
+                                     "values are incomplete")
                 _raise_geometry(key, lambda e, q: _device_error_detail(dd, e - base_index, q, stream))
     return values, (None if f is False else f)
+
+
+def _first_pattern_miss(element_nodes, row_ptr, col):
+    """Smallest local element index with a node pair the CSR pattern lacks, or None (torch, on
+    the device; only run on the rare path where a NEAR key could have hidden one)."""
+    import torch
+
+    n, ns = element_nodes.shape
+    if not n:
+        return None
+    n_nodes = row_ptr.numel() - 1
+    rows = torch.repeat_interleave(torch.arange(n_nodes, device=col.device), (row_ptr[1:] - row_ptr[:-1]).long())
+    have = rows * n_nodes + col.long()   # sorted when each row's columns are
+    have, _ = torch.sort(have)
+    nodes = element_nodes.long()
+    want = (nodes[:, :, None] * n_nodes + nodes[:, None, :]).reshape(n, -1)
+    pos = torch.searchsorted(have, want).clamp_(max=max(have.numel() - 1, 0))
+    ok = (have[pos] == want) if have.numel() else torch.zeros_like(want, dtype=torch.bool)
+    bad = (~ok).any(dim=1).nonzero()
+    return int(bad[0]) if bad.numel() else None

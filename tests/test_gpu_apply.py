@@ -141,3 +141,43 @@ def test_assemble_matches_oracle(et, pb, spec):
     y2 = (csr @ torch.from_numpy(x).cuda().unsqueeze(1)).squeeze(1)
     _, _, ym, _ = _scatter(A, b, nodes, x, nn)
     assert bool(((y - y2).abs().cpu() <= torch.from_numpy(2e-13 * ym + 1e-300)).all())
+
+
+@pytest.mark.parametrize("et,pb,spec", CASES[::2], ids=lambda c: getattr(c, "value", None) or str(getattr(c, "nx", c)))
+def test_assemble_reports_pattern_miss(et, pb, spec):
+    """A pattern lacking one node pair: the kernel skips that contribution (no write elsewhere) and
+    assemble_batch raises naming the first element that needs it; malformed structures are rejected."""
+    geo, cof, nodes, x = _setup(et, pb, spec)
+    desc = KernelDescriptor(Variant.QSS, fek.natural_path(et), pb, et)
+    nn = len(x)
+    dev = DeviceBatch.from_host(ElementBatch.from_arrays(et, pb, geo, cof))
+    tn = torch.from_numpy(nodes).cuda()
+    row_ptr, col = fek.csr_pattern(tn, nn)
+    rp, cl = row_ptr.cpu().numpy().astype(np.int64), col.cpu().numpy()
+    # drop the pair (i, j) of element 57's rows 1 and 2 from row i
+    i, j = int(nodes[57, 1]), int(nodes[57, 2])
+    k = rp[i] + int(np.searchsorted(cl[rp[i]:rp[i + 1]], j))
+    assert cl[k] == j
+    cl2 = np.delete(cl, k)
+    rp2 = rp.copy()
+    rp2[i + 1:] -= 1
+    first = min(e for e in range(len(nodes)) if i in nodes[e] and j in nodes[e])
+    values = torch.full((len(cl2),), 0.0, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError, match=f"element {first}"):
+        fek.assemble_batch(desc, dev, tn, torch.from_numpy(rp2.astype(np.int32)).cuda(),
+                           torch.from_numpy(cl2).cuda(), values)
+    # the entries that remain match a full assembly's (nothing landed in a neighbour's slot)
+    full, _ = fek.assemble_batch(desc, dev, tn, row_ptr, col)
+    keep = np.ones(len(cl), bool)
+    keep[k] = False
+    got, ref = values.cpu().numpy(), full.cpu().numpy()[keep]
+    assert np.allclose(got, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+    # malformed structures
+    bad = rp.astype(np.int32).copy()
+    bad[-1] -= 1
+    with pytest.raises(ValueError, match="row_ptr"):
+        fek.assemble_batch(desc, dev, tn, torch.from_numpy(bad).cuda(), col)
+    badc = cl.copy()
+    badc[3] = nn
+    with pytest.raises(ValueError, match="col"):
+        fek.assemble_batch(desc, dev, tn, row_ptr, torch.from_numpy(badc).cuda())

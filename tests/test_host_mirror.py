@@ -230,3 +230,24 @@ def test_bind_exception_types_makes_the_boundary_raise_host_classes():
             setattr(errors, n, cls)
     with pytest.raises(fek.InvertedElement):
         batched._raise_geometry((17, 3, 2), lambda e, q: (-0.5, 1e-14))
+
+
+def test_first_pattern_miss_on_cpu():
+    """The rare-path pattern check of assemble_batch (torch; runs on CPU tensors too)."""
+    import torch
+
+    from paper_1504_01023_b200 import mesh
+    from paper_1504_01023_b200.kernels.apply import _first_pattern_miss, csr_pattern
+
+    spec = mesh.MeshSpec(4, 3, 2, mesh.ElementType.TETRAHEDRON)
+    nodes = torch.from_numpy(mesh.element_nodes(spec))
+    nn = mesh.node_count(spec)
+    row_ptr, col = csr_pattern(nodes, nn)
+    assert _first_pattern_miss(nodes, row_ptr, col) is None
+    rp, cl = row_ptr.long(), col.clone()
+    i, j = int(nodes[7, 0]), int(nodes[7, 3])
+    k = int(rp[i]) + int(torch.searchsorted(cl[rp[i]:rp[i + 1]].contiguous(), j))
+    cl = torch.cat([cl[:k], cl[k + 1:]])
+    rp[i + 1:] -= 1
+    first = min(e for e in range(len(nodes)) if i in nodes[e].tolist() and j in nodes[e].tolist())
+    assert _first_pattern_miss(nodes, rp.int(), cl) == first
