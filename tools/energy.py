@@ -78,10 +78,18 @@ def main():
         return joules / dt
 
     idle = run("idle", [], 0)
+    # HBM energy per byte: a device-to-device copy of 2 GiB (read + write bytes)
+    src = torch.empty(1 << 28, dtype=torch.float64, device="cuda")
+    dst = torch.empty_like(src)
+    moved = 2 * src.numel() * 8
+    w_copy = run("copy", [lambda: dst.copy_(src)], moved)  # "elements" = bytes moved
+    del src, dst
+    torch.cuda.empty_cache()
     for p in parts:
         run(p.cfg.key, [p.L], p.n)
     run("C5", [p.L for p in parts], sum(p.n for p in parts))
-    print(f"(idle board power {idle:.0f} W included in every figure)")
+    print(f"(idle board power {idle:.0f} W included in every figure; for `copy` the 'elements' are bytes moved, "
+          f"so nJ/element there is nJ per byte)")
 
 
 if __name__ == "__main__":
